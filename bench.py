@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the DARE hot paths on B200 (BASELINE.json metric:
+"reslices/sec and p50 reslice latency; recon input Mpix/sec; % HBM roofline").
+
+Workload (N=1): BASELINE.json configs[1], cfg2 -- 1000 frames 512x512 -> 256^3
+directional grid, reslices at 256x256 (SURVEY Appendix B geometry, synthetic
+content).  A step = one batch of B=64 reslice poses through the device path.
+
+  value      reslices/s over all ranks, inputs (volume, pose params) resident
+             in HBM, CUDA events on the launching stream, max over ranks
+  e2e        reslices/s through the C ABI host-buffer call (dare_reslice):
+             per step H2D of 64 x 14 f64 pose params and D2H of pixels+coverage
+  latency    p50/p95 of single-pose reslice() through the public API
+  recon      reconstruct_volume input Mpix/s (frames in HBM, and e2e from pinned host)
+  roofline   dominant kernel (reslice_k) algorithmic bytes (SURVEY §8d
+             reference-layout formula) / measured step time vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline  CPU oracle (oracle/, C + OpenMP) on a bounded sample (slab oracle)
+
+`--impl reference` times the reference's CPU algorithm (the oracle port; the
+reference is pure Python/numba and is not installed on the GPU box) on the same
+config, rank 0 only.  Multi-GPU (torchrun): every rank builds its replica of
+the volume and reslices its own poses (pose-sharded, no data-path collective;
+scaling "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bench_data  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="cfg2", choices=sorted(bench_data.CONFIGS))
+    p.add_argument("--batch", type=int, default=0, help="poses per step (default: config's)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+class DevArray:
+    """__cuda_array_interface__ view of a raw device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), True),
+                                         "version": 2}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def cells_visited(torch, dims, origin, voxel, p14, W, H, radius):
+    dev = "cuda"
+    u = torch.arange(W, device=dev, dtype=torch.float64)
+    v = torch.arange(H, device=dev, dtype=torch.float64)
+    du = (u * p14[12])[None, :]
+    dv = (v * p14[13])[:, None]
+    inv_v = 1.0 / voxel
+    lo, hi = [], []
+    for a, (ci, cj) in enumerate(((3, 4), (6, 7), (9, 10))):
+        w = (p14[a] + du * p14[ci]) + dv * p14[cj]
+        l = torch.floor(((w - radius) - origin[a]) * inv_v - 1e-9).clamp(min=0)
+        h = torch.floor(((w + radius) - origin[a]) * inv_v + 1e-9).clamp(max=dims[a] - 1)
+        lo.append(l.reshape(-1).long())
+        hi.append(h.reshape(-1).long())
+    span = [int((hi[a] - lo[a]).max().item()) + 1 for a in range(3)]
+    cells = []
+    for ox in range(max(span[0], 0)):
+        for oy in range(max(span[1], 0)):
+            for oz in range(max(span[2], 0)):
+                cx, cy, cz = lo[0] + ox, lo[1] + oy, lo[2] + oz
+                ok = (cx <= hi[0]) & (cy <= hi[1]) & (cz <= hi[2])
+                lin = (cx * dims[1] + cy) * dims[2] + cz
+                cells.append(lin[ok])
+    if not cells:
+        return torch.empty(0, dtype=torch.long, device=dev)
+    return torch.unique(torch.cat(cells))
+
+
+def make_rank_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+
+def oracle_sample(wl, sweep, frames_np, plane_list, cfg, gpu_pixels=None):
+    """Slab-oracle reslice of a few poses on the host cores -> (ms per pose list, parity flags)."""
+    from oracle import oracle
+
+    frames = oracle.frame_poses(sweep)
+    origin, voxel, dims = oracle.grid(frames, wl.size, wl.size, sweep.pixel_pitch, wl.voxel, 0.0)
+    cfga = oracle.cfg_array(cfg)
+    times, parity = [], []
+    for k, plane in enumerate(plane_list):
+        p = oracle.plane_params(plane)
+        # z extent of the cells this plane can visit (identity-rotation sweep: frame k at z_k)
+        corners = [np.array([p[0], p[1], p[2]]) + a * np.array([p[3], p[6], p[9]]) + b * np.array([p[4], p[7], p[10]])
+                   for a in (0, (plane.width - 1) * p[12]) for b in (0, (plane.height - 1) * p[13])]
+        zs = [c[2] for c in corners]
+        zlo = math.floor(((min(zs) - cfg.interp_radius) - origin[2]) / voxel) - 2
+        zhi = math.floor(((max(zs) + cfg.interp_radius) - origin[2]) / voxel) + 2
+        sub = [f for f in frames
+               if zlo * voxel + origin[2] - voxel <= f.trans[2] <= (zhi + 1) * voxel + origin[2] + voxel]
+        vol = oracle.reconstruct_subset(sweep, sub, origin, voxel, dims)
+        t0 = time.perf_counter()
+        px, cov = oracle.reslice(vol, p, cfga, plane.width, plane.height, cfg.unassigned_value)
+        times.append((time.perf_counter() - t0) * 1000.0)
+        if gpu_pixels is not None:
+            parity.append(bool(np.array_equal(px, gpu_pixels[0][k]) and np.array_equal(cov, gpu_pixels[1][k])))
+    return times, parity
+
+
+def host_sweep(wl, frames_np):
+    from types import SimpleNamespace
+
+    from paper_2605_26325_b200.geometry import Pose
+
+    poses, ts = bench_data.sweep_poses(wl)
+    return SimpleNamespace(images=frames_np, image_timestamps=ts, pose_timestamps=ts.copy(), poses=poses,
+                           pixel_pitch=(wl.pitch, wl.pitch), calibration=Pose.identity(), mask=None)
+
+
+def run_reference(args):
+    """Reference arm: the reference's CPU algorithm (oracle port) on this box's host cores."""
+    ws, rank, _ = make_rank_info()
+    if rank != 0:
+        return
+    from paper_2605_26325_b200.reslice import ResliceConfig
+
+    wl = bench_data.workload(args.config)
+    frames_np = bench_data.render_frames_numpy(wl)
+    sweep = host_sweep(wl, frames_np)
+    cfg = ResliceConfig(interp_radius=wl.voxel)
+    planes = bench_data.reslice_planes(wl, args.warmup + args.steps)
+    from oracle import oracle
+
+    t0 = time.perf_counter()
+    vol = oracle.reconstruct(sweep, wl.voxel, 0.0)  # full volume, built once (setup, untimed)
+    setup_s = time.perf_counter() - t0
+    cfga = oracle.cfg_array(cfg)
+    for plane in planes[: args.warmup]:
+        oracle.reslice(vol, oracle.plane_params(plane), cfga, plane.width, plane.height)
+    times = []
+    for plane in planes[args.warmup:]:
+        p = oracle.plane_params(plane)
+        t0 = time.perf_counter()
+        oracle.reslice(vol, p, cfga, plane.width, plane.height)
+        times.append((time.perf_counter() - t0) * 1000.0)
+    ms = statistics.mean(times)
+    value = 1000.0 / ms
+    cores = os.cpu_count()
+    out = {
+        "impl": "reference", "metric": "reslices/sec", "value": value, "unit": "reslices/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "p50_reslice_ms": statistics.median(times),
+        "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> "
+                               f"{wl.voxel} mm grid, 1 pose/step at {wl.plane}x{wl.plane}",
+                   "parallelism": "host threads (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": "reslices/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} single-pose reslices of the full {args.config} volume "
+                                   f"(oracle reconstruct, untimed setup {setup_s:.0f} s)"},
+        "e2e": {"value": value, "unit": "reslices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ----------------------------------------------------------------------------- B200 arm
+
+def run_b200(args):
+    import torch
+
+    import paper_2605_26325_b200 as db
+    from paper_2605_26325_b200 import _lib
+    from paper_2605_26325_b200.reslice import ResliceConfig, kernel_cfg, plane_params
+
+    ws, rank, local = make_rank_info()
+    torch.cuda.set_device(local)
+    _lib.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    wl = bench_data.workload(args.config)
+    B = args.batch or wl.batch
+    cfg = ResliceConfig(interp_radius=wl.voxel)
+
+    # ---- reconstruction (every rank builds its replica) ----
+    frames_d = bench_data.render_frames_torch(wl)
+    torch.cuda.synchronize()
+    poses, ts = bench_data.sweep_poses(wl)
+    from types import SimpleNamespace
+
+    from paper_2605_26325_b200.geometry import Pose
+
+    dev_sweep = SimpleNamespace(images=frames_d, image_timestamps=ts, pose_timestamps=ts.copy(), poses=poses,
+                                pixel_pitch=(wl.pitch, wl.pitch), calibration=Pose.identity(), mask=None)
+    npix = wl.n_frames * wl.size * wl.size
+    db.reconstruct_volume(dev_sweep, voxel_size=wl.voxel, margin=0.0)  # warm-up (allocator pools, modules)
+    recon_ms = []
+    vol = None
+    for _ in range(3):
+        del vol
+        barrier()
+        t0 = time.perf_counter()
+        vol = db.reconstruct_volume(dev_sweep, voxel_size=wl.voxel, margin=0.0)
+        recon_ms.append((time.perf_counter() - t0) * 1000.0)
+    recon_dev_ms = max_over_ranks(min(recon_ms))
+    frames_pinned = frames_d.cpu().pin_memory()
+    frames_np = frames_pinned.numpy()
+    host_sw = host_sweep(wl, frames_np)
+    barrier()
+    t0 = time.perf_counter()
+    vol_e2e = db.reconstruct_volume(host_sw, voxel_size=wl.voxel, margin=0.0)
+    recon_e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1000.0)
+    del vol_e2e
+    info = vol.device_info()
+
+    # ---- reslice poses ----
+    planes = bench_data.reslice_planes(wl, (args.warmup + args.steps) * B, seed=rank)
+    params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
+    params_d = torch.from_numpy(params).cuda()
+    H = W = wl.plane
+    out_d = torch.empty((2, B, H, W), dtype=torch.uint8, device="cuda")
+    kc = kernel_cfg(cfg)
+    stream = torch.cuda.current_stream()
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    handle = vol.device_handle().raw
+
+    def launch(step):
+        pp = params_d[step * B:(step + 1) * B]
+        _lib.call("dare_reslice_device", handle, B, ctypes.c_void_p(pp.data_ptr()), W, H, ctypes.byref(kc),
+                  ctypes.c_void_p(out_d[0].data_ptr()), ctypes.c_void_p(out_d[1].data_ptr()), sptr)
+
+    for s in range(args.warmup):
+        launch(s)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.steps):
+        launch(args.warmup + s)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_per_step = dev_ms / args.steps
+    value = ws * B * args.steps / (dev_ms / 1000.0)
+
+    # ---- e2e through the C ABI with host buffers ----
+    params_pin = torch.from_numpy(params).pin_memory().numpy()
+    px_pin = torch.empty((B, H, W), dtype=torch.uint8).pin_memory().numpy()
+    cov_pin = torch.empty((B, H, W), dtype=torch.uint8).pin_memory().numpy()
+
+    def host_call(step):
+        pp = params_pin[step * B:(step + 1) * B]
+        _lib.call("dare_reslice", handle, B, pp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), W, H,
+                  ctypes.byref(kc), px_pin.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                  cov_pin.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+
+    for s in range(min(args.warmup, 3)):
+        host_call(s)
+    barrier()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        host_call(args.warmup + s)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = ws * B * args.steps / e2e_s
+
+    # ---- p50 single-pose latency through the public API ----
+    lat = []
+    for p in planes[:10]:
+        db.reslice(vol, p, cfg)
+    for p in planes[: max(100, args.steps)]:
+        lat.append(db.reslice(vol, p, cfg).timing_ms)
+    p50, p95 = float(np.percentile(lat, 50)), float(np.percentile(lat, 95))
+
+    # ---- roofline of reslice_k ----
+    offsets = torch.as_tensor(DevArray(info.d_cell_offsets, (int(np.prod(info.dims)) + 1,), "<i4"), device="cuda")
+    counts = (offsets[1:].long() - offsets[:-1].long())
+    dims = tuple(int(d) for d in info.dims)
+    origin = tuple(float(o) for o in info.origin)
+    ref_bytes = own_bytes = 0.0
+    visits = 0
+    step0 = args.warmup
+    for k in range(B):
+        p14 = params[step0 * B + k]
+        cells = cells_visited(torch, dims, origin, float(info.voxel_size), p14, W, H, cfg.interp_radius)
+        c = counts[cells]
+        ref_bytes += 12 * len(cells) + 29 * float(c.sum().item()) + H * W * (1 + 1 / 8)
+        own_bytes += 4 * len(cells) + 16 * float(c.sum().item()) + H * W * 2
+    peak, peak_kind = hbm_peak()
+    achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
+
+    # ---- CPU baseline (rank 0, bounded sample) ----
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        sample_planes = planes[step0 * B: step0 * B + 2]
+        gp, gc, _ = db.reslice_batch(vol, sample_planes, cfg)
+        t_ms, parity = oracle_sample(wl, host_sw, frames_np, sample_planes, cfg, (gp, gc))
+        cpu = {"value": 1000.0 / statistics.mean(t_ms), "unit": "reslices/s", "cores": os.cpu_count(),
+               "kind": "port", "sample": "2 single-pose 256x256 reslices on a slab-oracle volume "
+                                         "(frames near each plane, full grid), C+OpenMP",
+               "parity_with_gpu": all(parity)}
+
+    if rank == 0:
+        out = {
+            "metric": "reslices/sec", "value": value, "unit": "reslices/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> dims {dims} "
+                                   f"({info.n_samples} samples), {B} poses/step at {W}x{H}, r={cfg.interp_radius}",
+                       "poses_per_step": B, "parallelism": f"pose-sharded x{ws} (replicated volume)",
+                       "l2": "inputs larger than L2 (volume records "
+                             f"{info.n_samples * 16 / 1e9:.1f} GB; each step's poses touch "
+                             f"{own_bytes / 1e9:.2f} GB)"},
+            "p50_reslice_ms": p50, "p95_reslice_ms": p95,
+            "recon": {"metric": "recon input Mpix/s", "value": ws * npix / 1e6 / (recon_dev_ms / 1000.0),
+                      "ms": recon_dev_ms, "e2e_value": ws * npix / 1e6 / (recon_e2e_ms / 1000.0),
+                      "e2e_ms": recon_e2e_ms, "input_pixels": npix, "samples": int(info.n_samples),
+                      "note": "wall time of the C-ABI call (frames in HBM / from pinned host), incl. host syncs"},
+            "e2e": {"value": e2e_value, "unit": "reslices/s", "h2d_bytes_per_step": B * 14 * 8,
+                    "d2h_bytes_per_step": 2 * B * H * W},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "reslice_k (+gate_k)",
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_step_ref_layout": ref_bytes,
+                         "compulsory_bytes_per_step_own_layout": own_bytes},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

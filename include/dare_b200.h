@@ -1,0 +1,204 @@
+/*
+ * dare_b200.h -- C ABI of the B200-native DARE hot paths (libdare_b200.so).
+ *
+ * Drop-in seam for the reference package `dare` (arxiv/paper_2605_26325,
+ * pkg/src/dare/).  The reference is pure Python; its operator seam is the
+ * numba kernels in _kernels.py plus the vectorised numpy blocks of
+ * VolumeBuilder / compound / fill_holes.  Each entry point below names the
+ * reference interface it replaces.  Plain pointers, sizes and opaque handles
+ * only (no torch / C++ types); a ctypes binding is in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every function returns 0 on success or a negative dare_status; the
+ *    message is available from dare_last_error() (thread-local).
+ *  - Preconditions that the reference checks in Python (unit-norm plane
+ *    rotation, radius > 0, ...) are validated by the Python host layer before
+ *    any call; these functions check only memory/shape consistency.
+ *  - Host-computed f64 parameters are passed by value / host arrays so their
+ *    bits are exactly what Python computed.
+ *  - Re-entrant: concurrent calls on one (immutable) volume handle from many
+ *    threads are safe; each calling thread gets its own CUDA stream.
+ *  - `*_device` variants take device pointers and an explicit cudaStream_t
+ *    (passed as void*) and do not synchronise; plain variants take host
+ *    buffers, copy in/out and return when results are on the host.
+ *
+ * Plane parameters (14 doubles per pose, reslice.py:135-148 `_plane_params`):
+ *   tx, ty, tz, r00, r01, r02, r10, r11, r12, r20, r21, r22, pitch_x, pitch_y
+ * with R the (un-renormalised) plane rotation matrix, row-major.
+ *
+ * Frame axes (9 doubles per synchronized frame, reconstruct.py:152-163):
+ *   R[0][0], R[1][0], R[2][0]   (image x axis  = R[:,0])
+ *   R[0][1], R[1][1], R[2][1]   (image y axis  = R[:,1])
+ *   tx, ty, tz                  (frame translation)
+ */
+#ifndef DARE_B200_H
+#define DARE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DARE_OK = 0,
+  DARE_ERR_INVALID = -1, /* bad argument / shape */
+  DARE_ERR_CUDA = -2,    /* CUDA runtime error */
+  DARE_ERR_NOMEM = -3,   /* device or host allocation failed */
+  DARE_ERR_LIMIT = -4    /* input exceeds a documented layout limit */
+} dare_status;
+
+typedef struct dare_volume_s* dare_volume_t; /* sealed DirectionalVolume on one device */
+typedef struct dare_scalar_s* dare_scalar_t; /* ScalarVolume on one device */
+
+/* reslice.py:63-100 ResliceConfig, already reduced to kernel scalars
+ * (cos_* = math.cos(math.radians(deg)) computed by the caller). */
+typedef struct {
+  double radius;
+  double cos_normal;
+  double cos_inplane;
+  double k_normal;
+  double k_inplane;
+  double k_dist;
+  int32_t unassigned;
+  int32_t _pad;
+} dare_reslice_cfg;
+
+typedef struct {
+  int32_t device;
+  int32_t _pad;
+  double origin[3];
+  double voxel_size;
+  int64_t dims[3];
+  int64_t n_samples;
+  int64_t n_orientations;
+  int64_t rejected_out_of_bounds;
+  /* device pointers (read-only views, owned by the handle) */
+  const uint32_t* d_cell_offsets; /* ncells + 1 exclusive prefix of counts */
+  const void* d_records;          /* n_samples x 16 B: f32 x,y,z, u32 (oid<<8 | intensity) */
+  const float* d_orientations;    /* n_orientations x 4 f32 (w,x,y,z), canonical */
+  size_t device_bytes;
+} dare_volume_info;
+
+typedef struct {
+  int32_t device;
+  int32_t _pad;
+  double origin[3];
+  double voxel_size;
+  int64_t dims[3];
+  float* d_values;   /* ncells f32 */
+  uint8_t* d_flags;  /* ncells u8: 0 empty, 1 observed, 2 filled */
+  int64_t* d_counts; /* ncells i64 observation counts, or NULL */
+} dare_scalar_info;
+
+/* ---- runtime ------------------------------------------------------------ */
+const char* dare_last_error(void);
+int dare_version(void);
+int dare_get_device_count(int32_t* count);
+int dare_set_device(int32_t device);
+int dare_synchronize(void);
+int dare_host_alloc(size_t bytes, void** ptr); /* pinned host memory */
+int dare_host_free(void* ptr);
+int dare_device_alloc(size_t bytes, void** ptr);
+int dare_device_free(void* ptr);
+int dare_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* cudaMemcpyDefault */
+int dare_stream_sync(void* stream);
+
+/* ---- directional volume ------------------------------------------------- */
+
+/* Replaces reconstruct.py:166-199 reconstruct_volume's per-frame scatter
+ * (reconstruct.py:186-196, frame_world_positions 152-163, VolumeBuilder
+ * insert_batch/_voxel_indices volume.py:208-238) and VolumeBuilder.seal
+ * (volume.py:240-269).  `frames` is the (n_images, H, W) u8 stack (host or
+ * device, see frames_on_device); frame_image[i] selects the image of the i-th
+ * synchronized frame; axes/quats are per synchronized frame; mask (H*W u8,
+ * host) or NULL.  Builds the sealed CSR volume on the current device and
+ * reports the out-of-bounds count (volume.py:230-233). */
+int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t height, int32_t width,
+                     int32_t frames_on_device, const int32_t* frame_image, int64_t n_frames,
+                     const double* frame_axes, const float* frame_quats, double pitch_x,
+                     double pitch_y, const uint8_t* mask, const double* origin, double voxel_size,
+                     const int64_t* dims, dare_volume_t* out, int64_t* rejected_out_of_bounds);
+
+/* Replaces VolumeBuilder.seal (volume.py:240-269) for arbitrary samples
+ * (VolumeBuilder.insert_sample/insert_batch inputs, volume.py:211-238):
+ * positions f32[n,3], orientations f32[n,4], intensities u8[n] in insertion
+ * order (host).  Stable by insertion order within each cell, like numpy's
+ * argsort(kind="stable"); out-of-bounds samples are dropped. */
+int dare_volume_seal(const double* origin, double voxel_size, const int64_t* dims,
+                     int64_t n_samples, const float* positions, const float* orientations,
+                     const uint8_t* intensities, dare_volume_t* out);
+
+/* Uploads a sealed volume in the reference layout (volume.py:76-93, as
+ * produced by VolumeBuilder.seal or load_volume volume.py:300-330):
+ * cell_starts/cell_counts i64[ncells], positions f32[n,3], orientations
+ * f32[n,4], intensities u8[n] (host). */
+int dare_volume_upload(const double* origin, double voxel_size, const int64_t* dims,
+                       const int64_t* cell_starts, const int64_t* cell_counts, int64_t n_samples,
+                       const float* positions, const float* orientations,
+                       const uint8_t* intensities, dare_volume_t* out);
+
+/* Materialises the reference layout on the host (buffers sized per info). */
+int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int64_t* cell_counts,
+                         float* positions, float* orientations, uint8_t* intensities);
+int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info);
+int dare_volume_destroy(dare_volume_t vol);
+
+/* Replaces reslice.py:168-187 reslice -> _run_rows -> _kernels.reslice_rows_grid
+ * (_kernels.py:84-139, _accumulate_run 29-68, _finalize_pixel 71-81), batched
+ * over n_poses planes of one raster size.  params: n_poses x 14 doubles.
+ * pixels/coverage: n_poses x height x width u8 (coverage 0/1).  Host buffers. */
+int dare_reslice(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
+                 int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
+                 uint8_t* coverage);
+/* Contract twin of reslice (reslice.py:190-205 -> _kernels.reslice_rows_bruteforce
+ * 142-167): every sample in storage order for every pixel.  Host buffers. */
+int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const double* params,
+                            int32_t width, int32_t height, const dare_reslice_cfg* cfg,
+                            uint8_t* pixels, uint8_t* coverage);
+/* Same on device buffers (params, pixels, coverage device pointers). */
+int dare_reslice_device(dare_volume_t vol, int32_t n_poses, const double* d_params,
+                        int32_t width, int32_t height, const dare_reslice_cfg* cfg,
+                        uint8_t* d_pixels, uint8_t* d_coverage, void* stream);
+
+/* ---- scalar (direction-blind) arm -------------------------------------- */
+
+/* Replaces baseline.py:64-97 compound (np.add.at scatter + mean). Arguments
+ * as dare_reconstruct. */
+int dare_compound(const uint8_t* frames, int64_t n_images, int32_t height, int32_t width,
+                  int32_t frames_on_device, const int32_t* frame_image, int64_t n_frames,
+                  const double* frame_axes, double pitch_x, double pitch_y, const uint8_t* mask,
+                  const double* origin, double voxel_size, const int64_t* dims,
+                  dare_scalar_t* out);
+/* Uploads values f32 / flags u8 / counts i64 (counts may be NULL). */
+int dare_scalar_upload(const double* origin, double voxel_size, const int64_t* dims,
+                       const float* values, const uint8_t* flags, const int64_t* counts,
+                       dare_scalar_t* out);
+int dare_scalar_download(dare_scalar_t vol, float* values, uint8_t* flags, int64_t* counts);
+int dare_scalar_get_info(dare_scalar_t vol, dare_scalar_info* info);
+int dare_scalar_destroy(dare_scalar_t vol);
+
+/* Replaces baseline.py:100-127 fill_holes (Jacobi passes, bit-exact). Returns
+ * a new handle; *passes_run = passes that filled at least one voxel. */
+int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar_t* out,
+                    int32_t* passes_run);
+
+/* Replaces baseline.py:130-155 reslice_trilinear -> _kernels.trilinear_rows
+ * (_kernels.py:170-229), batched.  values (optional, may be NULL) receives the
+ * pre-rounding f64 value per pixel.  Host buffers. */
+int dare_reslice_trilinear(dare_scalar_t vol, int32_t n_poses, const double* params,
+                           int32_t width, int32_t height, uint8_t* pixels, uint8_t* coverage,
+                           double* values);
+int dare_reslice_trilinear_device(dare_scalar_t vol, int32_t n_poses, const double* d_params,
+                                  int32_t width, int32_t height, uint8_t* d_pixels,
+                                  uint8_t* d_coverage, double* d_values, void* stream);
+
+/* ---- diagnostics -------------------------------------------------------- */
+/* Device restatement of glibc exp on n device doubles (parity tests). */
+int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DARE_B200_H */

@@ -1,0 +1,133 @@
+// Shared runtime plumbing for libdare_b200.so: status/error reporting,
+// per-thread streams, stream-ordered scratch, and the exact-arithmetic
+// helpers every kernel uses.  The whole library is compiled with -fmad=false
+// so no multiply-add is ever contracted (the reference never fuses either).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/dare_b200.h"
+
+namespace dare {
+
+void set_error(const std::string& msg);
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define DARE_CUDA(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      throw ::dare::Error{DARE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e) + \
+                                             " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+    }                                                                                    \
+  } while (0)
+
+#define DARE_REQUIRE(cond, msg)                                   \
+  do {                                                            \
+    if (!(cond)) throw ::dare::Error{DARE_ERR_INVALID, (msg)};    \
+  } while (0)
+
+#define DARE_LIMIT(cond, msg)                                     \
+  do {                                                            \
+    if (!(cond)) throw ::dare::Error{DARE_ERR_LIMIT, (msg)};      \
+  } while (0)
+
+// Runs `body`, converting exceptions into a status code + thread-local message.
+template <class F>
+int guard(F&& body) {
+  try {
+    body();
+    return DARE_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return DARE_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return DARE_ERR_INVALID;
+  }
+}
+
+// One non-blocking stream per (host thread, device): concurrent reslice calls
+// from different threads never serialise on a shared stream.
+cudaStream_t thread_stream();
+
+// Stream-ordered device scratch (cudaMallocAsync pool) freed on scope exit.
+template <class T>
+struct Scratch {
+  T* ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  Scratch() = default;
+  Scratch(size_t n, cudaStream_t s) : stream(s) {
+    if (n) DARE_CUDA(cudaMallocAsync((void**)&ptr, n * sizeof(T), s));
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+// True when 1/x is exactly representable, so (y / x) == (y * (1/x)) bit-for-bit
+// (both are the correctly rounded value of the same real number).
+inline bool exact_reciprocal(double x) {
+  if (!(x > 0.0) || x > 1e300 || x < 1e-300) return false;
+  int e;
+  double m = frexp(x, &e);
+  return m == 0.5;
+}
+
+int sm_count();
+
+}  // namespace dare
+
+// ---- device helpers ------------------------------------------------------
+
+// The reference's voxel-index chain `floor((f64(p32) - origin) / voxel)`
+// (volume.py:209).  When voxel is a power of two the division is replaced by
+// the exact reciprocal multiply (identical result, far cheaper on the FP64 pipe).
+struct VoxelMap {
+  double origin[3];
+  double voxel;
+  double inv_voxel;
+  int exact_inv;
+  int64_t dims[3];
+};
+
+__device__ __forceinline__ double voxel_coord(const VoxelMap& m, int a, float p32) {
+  double d = (double)p32 - m.origin[a];
+  return m.exact_inv ? d * m.inv_voxel : d / m.voxel;
+}
+
+// Pixel (u, v) of a frame with axes fa = {c0[3], c1[3], t[3]} ->
+// f32 world position (reconstruct.py:156-162) and linear cell (or -1 if out
+// of bounds; volume.py:229-230).
+__device__ __forceinline__ int64_t pixel_cell(const double* __restrict__ fa, int u, int v,
+                                              double px, double py, const VoxelMap& m,
+                                              float* p32) {
+  double U = (double)u * px;
+  double V = (double)v * py;
+  bool ok = true;
+  int64_t idx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double P = (U * fa[a] + V * fa[3 + a]) + fa[6 + a];
+    float f32 = __double2float_rn(P);
+    p32[a] = f32;
+    double f = floor(voxel_coord(m, a, f32));
+    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
+    idx[a] = ok ? (int64_t)f : 0;
+  }
+  return ok ? (idx[0] * m.dims[1] + idx[1]) * m.dims[2] + idx[2] : -1;
+}

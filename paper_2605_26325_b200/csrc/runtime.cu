@@ -1,0 +1,167 @@
+// Runtime entry points of the C ABI: errors, devices, streams, memory.
+#include <map>
+#include <mutex>
+
+#include "volume.cuh"
+
+namespace dare {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+cudaStream_t thread_stream() {
+  // One stream per (thread, device); destroyed with the thread.
+  struct Streams {
+    std::map<int, cudaStream_t> by_dev;
+    ~Streams() {
+      for (auto& kv : by_dev) cudaStreamDestroy(kv.second);
+    }
+  };
+  static thread_local Streams streams;
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
+  auto it = streams.by_dev.find(dev);
+  if (it != streams.by_dev.end()) return it->second;
+  cudaStream_t s;
+  DARE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  streams.by_dev[dev] = s;
+  return s;
+}
+
+int sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  DARE_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  cache[dev] = n;
+  return n;
+}
+
+VoxelMap make_voxel_map(const double* origin, double voxel, const int64_t* dims) {
+  VoxelMap m;
+  for (int a = 0; a < 3; ++a) {
+    m.origin[a] = origin[a];
+    m.dims[a] = dims[a];
+  }
+  m.voxel = voxel;
+  m.exact_inv = exact_reciprocal(voxel) ? 1 : 0;
+  m.inv_voxel = 1.0 / voxel;
+  return m;
+}
+
+FrameSet::FrameSet(const uint8_t* frames, int64_t n_images, int32_t H_, int32_t W_,
+                   int32_t on_device, const int32_t* frame_image, int64_t n_frames_,
+                   const double* axes, double px_, double py_, const uint8_t* mask,
+                   cudaStream_t s)
+    : n_frames(n_frames_), H(H_), W(W_), px(px_), py(py_), stream(s) {
+  DARE_REQUIRE(H > 0 && W > 0, "frame height and width must be positive");
+  DARE_REQUIRE(n_frames >= 0 && n_images >= 0, "negative frame count");
+  const size_t hw = (size_t)H * W;
+  for (int64_t i = 0; i < n_frames; ++i)
+    DARE_REQUIRE(frame_image[i] >= 0 && frame_image[i] < n_images, "frame_image index out of range");
+  if (on_device) {
+    d_frames = frames;
+  } else {
+    size_t bytes = hw * (size_t)n_images;
+    if (bytes) {
+      DARE_CUDA(cudaMallocAsync((void**)&owned_frames, bytes, s));
+      DARE_CUDA(cudaMemcpyAsync(owned_frames, frames, bytes, cudaMemcpyHostToDevice, s));
+    }
+    d_frames = owned_frames;
+  }
+  if (n_frames) {
+    DARE_CUDA(cudaMallocAsync((void**)&d_image, sizeof(int32_t) * n_frames, s));
+    DARE_CUDA(cudaMemcpyAsync(d_image, frame_image, sizeof(int32_t) * n_frames,
+                              cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaMallocAsync((void**)&d_axes, sizeof(double) * 9 * n_frames, s));
+    DARE_CUDA(cudaMemcpyAsync(d_axes, axes, sizeof(double) * 9 * n_frames,
+                              cudaMemcpyHostToDevice, s));
+  }
+  if (mask) {
+    DARE_CUDA(cudaMallocAsync((void**)&d_mask, hw, s));
+    DARE_CUDA(cudaMemcpyAsync(d_mask, mask, hw, cudaMemcpyHostToDevice, s));
+  }
+}
+
+FrameSet::~FrameSet() {
+  if (owned_frames) cudaFreeAsync(owned_frames, stream);
+  if (d_image) cudaFreeAsync(d_image, stream);
+  if (d_axes) cudaFreeAsync(d_axes, stream);
+  if (d_mask) cudaFreeAsync(d_mask, stream);
+}
+
+}  // namespace dare
+
+dare_volume_s::~dare_volume_s() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (d_offsets) cudaFree(d_offsets);
+  if (d_records) cudaFree(d_records);
+  if (d_orient) cudaFree(d_orient);
+  cudaSetDevice(prev);
+}
+
+dare_scalar_s::~dare_scalar_s() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (d_values) cudaFree(d_values);
+  if (d_flags) cudaFree(d_flags);
+  if (d_counts) cudaFree(d_counts);
+  cudaSetDevice(prev);
+}
+
+using namespace dare;
+
+extern "C" {
+
+const char* dare_last_error(void) { return g_last_error.c_str(); }
+
+int dare_version(void) { return 100; }
+
+int dare_get_device_count(int32_t* count) {
+  return guard([&] {
+    int n = 0;
+    DARE_CUDA(cudaGetDeviceCount(&n));
+    *count = n;
+  });
+}
+
+int dare_set_device(int32_t device) { return guard([&] { DARE_CUDA(cudaSetDevice(device)); }); }
+
+int dare_synchronize(void) { return guard([&] { DARE_CUDA(cudaDeviceSynchronize()); }); }
+
+int dare_host_alloc(size_t bytes, void** ptr) {
+  return guard([&] { DARE_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocPortable)); });
+}
+
+int dare_host_free(void* ptr) { return guard([&] { DARE_CUDA(cudaFreeHost(ptr)); }); }
+
+int dare_device_alloc(size_t bytes, void** ptr) {
+  return guard([&] { DARE_CUDA(cudaMalloc(ptr, bytes)); });
+}
+
+int dare_device_free(void* ptr) { return guard([&] { DARE_CUDA(cudaFree(ptr)); }); }
+
+int dare_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
+  return guard([&] {
+    cudaStream_t s = stream ? (cudaStream_t)stream : thread_stream();
+    DARE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    if (!stream) DARE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int dare_stream_sync(void* stream) {
+  return guard([&] {
+    DARE_CUDA(cudaStreamSynchronize(stream ? (cudaStream_t)stream : thread_stream()));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,413 @@
+// Direction-blind (PLUS-style) comparison arm: compound -> fill_holes ->
+// reslice_trilinear.  Reference: baseline.py:64-155, _kernels.py:170-229.
+//
+//  compound  : same pixel -> cell map as reconstruction; u64 sum / u64 count
+//              atomics, warp-aggregated over equal cells (integer sums are
+//              order-free, so atomics are exact -- baseline.py:67 relies on it);
+//              then values = f32(f64(sum) / f64(count)) (baseline.py:93-96).
+//  fill_holes: Jacobi passes on an f64 working grid (baseline.py:108: values
+//              are promoted to f64 and filled values are NOT re-rounded between
+//              passes).  Neighbour sums run in C order over the 26 offsets (the
+//              order scipy's convolve visits the footprint), unknown and
+//              out-of-grid neighbours add 0.  In-place with pass tags: a voxel
+//              filled in pass p carries flag 3+p and is "unknown" to readers in
+//              pass p (Jacobi), "known" afterwards; finalize maps tags -> 2.
+//  trilinear : thread per pixel, 8 corners in (cx, cy, cz) order, f32 values
+//              read directly (the reference's per-call f64 copy of the whole
+//              grid, baseline.py:142-149, is pure overhead: f32->f64 is exact).
+#include <memory>
+#include <vector>
+
+#include "volume.cuh"
+
+namespace dare {
+
+struct ScalarFrameView {
+  const uint8_t* frames;
+  const int32_t* image;
+  const double* axes;
+  const uint8_t* mask;
+  int64_t n_frames;
+  int32_t H, W;
+  double px, py;
+};
+
+__global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m,
+                                                  unsigned long long* sums,
+                                                  unsigned long long* counts) {
+  __shared__ double s_axes[9];
+  const int64_t hw = (int64_t)fv.H * fv.W;
+  const unsigned lane = threadIdx.x & 31u;
+  for (int64_t f = blockIdx.y; f < fv.n_frames; f += gridDim.y) {
+    __syncthreads();
+    if (threadIdx.x < 9) s_axes[threadIdx.x] = fv.axes[f * 9 + threadIdx.x];
+    __syncthreads();
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool valid = p < hw;
+    if (valid && fv.mask) valid = fv.mask[p] != 0;
+    int64_t lin = -1;
+    unsigned inten = 0;
+    if (valid) {
+      float p32[3];
+      lin = pixel_cell(s_axes, (int)(p % fv.W), (int)(p / fv.W), fv.px, fv.py, m, p32);
+      inten = fv.frames[(size_t)fv.image[f] * hw + p];
+    }
+    bool kept = lin >= 0;
+    unsigned active = __ballot_sync(0xffffffffu, kept);
+    if (kept) {
+      unsigned peers = __match_any_sync(active, (unsigned long long)lin);
+      unsigned total = __reduce_add_sync(peers, inten);
+      if (lane == (unsigned)(__ffs(peers) - 1)) {
+        atomicAdd(&sums[lin], (unsigned long long)total);
+        atomicAdd(&counts[lin], (unsigned long long)__popc(peers));
+      }
+    }
+  }
+}
+
+__global__ void compound_finalize_k(int64_t n, const unsigned long long* __restrict__ sums,
+                                    const unsigned long long* __restrict__ counts, float* values,
+                                    uint8_t* flags) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  unsigned long long k = counts[c];
+  if (k > 0) {
+    values[c] = __double2float_rn((double)(long long)sums[c] / (double)(long long)k);
+    flags[c] = 1;
+  } else {
+    values[c] = 0.0f;
+    flags[c] = 0;
+  }
+}
+
+__global__ void to_f64_k(int64_t n, const float* __restrict__ v, double* w) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) w[c] = (double)v[c];
+}
+
+// known in pass p: observed (1), filled earlier (2 or a tag from pass < p)
+__device__ __forceinline__ bool known_in_pass(uint8_t f, int tag) { return f != 0 && f != tag; }
+
+__global__ void __launch_bounds__(256) fill_pass_k(int64_t nx, int64_t ny, int64_t nz,
+                                                   double* v, uint8_t* flags, int tag,
+                                                   unsigned long long* filled,
+                                                   const unsigned long long* prev_filled) {
+  if (prev_filled && *prev_filled == 0) return;  // previous pass changed nothing
+  const int64_t n = nx * ny * nz;
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool did = false;
+  if (c < n && flags[c] == 0) {
+    const int64_t z = c % nz, y = (c / nz) % ny, x = c / (ny * nz);
+    double s = 0.0, cnt = 0.0;
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int64_t X = x + dx;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int64_t Y = y + dy;
+        for (int dz = -1; dz <= 1; ++dz) {
+          if (dx == 0 && dy == 0 && dz == 0) continue;
+          const int64_t Z = z + dz;
+          double val = 0.0, k = 0.0;
+          if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
+            const int64_t q = (X * ny + Y) * nz + Z;
+            const uint8_t fq = ((volatile uint8_t*)flags)[q];
+            if (known_in_pass(fq, tag)) {
+              val = v[q];
+              k = 1.0;
+            }
+          }
+          s += val;
+          cnt += k;
+        }
+      }
+    }
+    if (cnt > 0.0) {
+      v[c] = s / cnt;
+      flags[c] = (uint8_t)tag;
+      did = true;
+    }
+  }
+  int any = __syncthreads_or(did);
+  if (threadIdx.x == 0 && any) atomicAdd(filled, 1ull);
+}
+
+__global__ void fill_finalize_k(int64_t n, const double* __restrict__ v, const uint8_t* flags_in,
+                                float* values, uint8_t* flags) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  uint8_t f = flags_in[c];
+  values[c] = __double2float_rn(v[c]);
+  flags[c] = f >= 3 ? 2 : f;
+}
+
+struct TrilinearArgs {
+  const float* values;
+  const uint8_t* flags;
+  const double* params;
+  double origin[3];
+  double voxel;
+  int64_t dims[3];
+  int W, H, tiles_x;
+};
+
+__global__ void __launch_bounds__(256) trilinear_k(TrilinearArgs a, uint8_t* out, uint8_t* cov,
+                                                   double* out_val) {
+  const int pose = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = (tile % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
+  const int v = (tile / a.tiles_x) * 16 + (warp >> 1) * 4 + (lane >> 3);
+  if (u >= a.W || v >= a.H) return;
+  const double* pp = a.params + (size_t)pose * 14;
+  const double du = (double)u * pp[12], dv = (double)v * pp[13];
+  const double w[3] = {(pp[0] + du * pp[3]) + dv * pp[4], (pp[1] + du * pp[6]) + dv * pp[7],
+                       (pp[2] + du * pp[9]) + dv * pp[10]};
+  const double inv_v = 1.0 / a.voxel;
+  int64_t i[3];
+  double fr[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double g = (w[k] - a.origin[k]) * inv_v - 0.5;
+    const double fl = floor(g);
+    const double lim = (double)a.dims[k] + 1.0;
+    i[k] = (int64_t)(fl < -2.0 ? -2.0 : (fl > lim ? lim : fl));
+    fr[k] = g - fl;
+  }
+  double wsum = 0.0, vsum = 0.0;
+  for (int cx = 0; cx < 2; ++cx) {
+    const int64_t jx = i[0] + cx;
+    if (jx < 0 || jx >= a.dims[0]) continue;
+    const double wxc = cx == 1 ? fr[0] : 1.0 - fr[0];
+    for (int cy = 0; cy < 2; ++cy) {
+      const int64_t jy = i[1] + cy;
+      if (jy < 0 || jy >= a.dims[1]) continue;
+      const double wyc = cy == 1 ? fr[1] : 1.0 - fr[1];
+      for (int cz = 0; cz < 2; ++cz) {
+        const int64_t jz = i[2] + cz;
+        if (jz < 0 || jz >= a.dims[2]) continue;
+        const int64_t lin = (jx * a.dims[1] + jy) * a.dims[2] + jz;
+        if (__ldg(a.flags + lin) != 0) {
+          const double wc = (wxc * wyc) * (cz == 1 ? fr[2] : 1.0 - fr[2]);
+          wsum += wc;
+          vsum += wc * (double)__ldg(a.values + lin);
+        }
+      }
+    }
+  }
+  const size_t k = ((size_t)pose * a.H + v) * a.W + u;
+  if (wsum >= 1e-12) {
+    const double val = vsum / wsum;
+    double r = floor(val + 0.5);
+    r = r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
+    out[k] = (uint8_t)r;
+    cov[k] = 1;
+    if (out_val) out_val[k] = val;
+  } else {
+    out[k] = 0;
+    cov[k] = 0;
+    if (out_val) out_val[k] = 0.0;
+  }
+}
+
+static std::unique_ptr<dare_scalar_s> new_scalar(const double* origin, double voxel,
+                                                  const int64_t* dims, bool with_counts) {
+  DARE_REQUIRE(voxel > 0, "voxel_size must be > 0");
+  DARE_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
+  auto sv = std::make_unique<dare_scalar_s>();
+  DARE_CUDA(cudaGetDevice(&sv->device));
+  for (int a = 0; a < 3; ++a) {
+    sv->origin[a] = origin[a];
+    sv->dims[a] = dims[a];
+  }
+  sv->voxel = voxel;
+  sv->ncells = dims[0] * dims[1] * dims[2];
+  DARE_CUDA(cudaMalloc(&sv->d_values, sizeof(float) * sv->ncells));
+  DARE_CUDA(cudaMalloc(&sv->d_flags, sv->ncells));
+  if (with_counts) DARE_CUDA(cudaMalloc(&sv->d_counts, sizeof(int64_t) * sv->ncells));
+  return sv;
+}
+
+static void launch_trilinear(dare_scalar_t vol, int32_t P, const double* d_params, int32_t W,
+                             int32_t H, uint8_t* d_pixels, uint8_t* d_cov, double* d_values,
+                             cudaStream_t s) {
+  DARE_REQUIRE(vol != nullptr, "null volume");
+  DARE_REQUIRE(W > 0 && H > 0, "reslice plane must have at least one pixel");
+  DARE_REQUIRE(P >= 0 && P <= 65535, "n_poses must be in [0, 65535] per launch");
+  if (P == 0) return;
+  TrilinearArgs a;
+  a.values = vol->d_values;
+  a.flags = vol->d_flags;
+  a.params = d_params;
+  for (int k = 0; k < 3; ++k) {
+    a.origin[k] = vol->origin[k];
+    a.dims[k] = vol->dims[k];
+  }
+  a.voxel = vol->voxel;
+  a.W = W;
+  a.H = H;
+  a.tiles_x = (int)ceil_div(W, 16);
+  trilinear_k<<<dim3(a.tiles_x * ceil_div(H, 16), P), 256, 0, s>>>(a, d_pixels, d_cov, d_values);
+  DARE_CUDA(cudaGetLastError());
+}
+
+}  // namespace dare
+
+using namespace dare;
+
+extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t height,
+                             int32_t width, int32_t frames_on_device, const int32_t* frame_image,
+                             int64_t n_frames, const double* frame_axes, double pitch_x,
+                             double pitch_y, const uint8_t* mask, const double* origin,
+                             double voxel_size, const int64_t* dims, dare_scalar_t* out) {
+  return guard([&] {
+    DARE_REQUIRE(out != nullptr, "out handle pointer is null");
+    cudaStream_t s = thread_stream();
+    FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
+                frame_axes, pitch_x, pitch_y, mask, s);
+    auto sv = new_scalar(origin, voxel_size, dims, true);
+    VoxelMap m = make_voxel_map(origin, voxel_size, dims);
+    Scratch<unsigned long long> sums(sv->ncells, s);
+    DARE_CUDA(cudaMemsetAsync(sums.ptr, 0, sizeof(unsigned long long) * sv->ncells, s));
+    DARE_CUDA(cudaMemsetAsync(sv->d_counts, 0, sizeof(int64_t) * sv->ncells, s));
+    ScalarFrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
+                       fs.H,        fs.W,       fs.px,     fs.py};
+    const int64_t hw = (int64_t)height * width;
+    if (n_frames > 0) {
+      dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(n_frames, 65535));
+      compound_k<<<grid, 256, 0, s>>>(fv, m, sums.ptr, (unsigned long long*)sv->d_counts);
+      DARE_CUDA(cudaGetLastError());
+    }
+    compound_finalize_k<<<ceil_div(sv->ncells, 256), 256, 0, s>>>(
+        sv->ncells, sums.ptr, (const unsigned long long*)sv->d_counts, sv->d_values, sv->d_flags);
+    DARE_CUDA(cudaGetLastError());
+    DARE_CUDA(cudaStreamSynchronize(s));
+    *out = sv.release();
+  });
+}
+
+extern "C" int dare_scalar_upload(const double* origin, double voxel_size, const int64_t* dims,
+                                  const float* values, const uint8_t* flags,
+                                  const int64_t* counts, dare_scalar_t* out) {
+  return guard([&] {
+    DARE_REQUIRE(out != nullptr, "out handle pointer is null");
+    auto sv = new_scalar(origin, voxel_size, dims, counts != nullptr);
+    cudaStream_t s = thread_stream();
+    DARE_CUDA(cudaMemcpyAsync(sv->d_values, values, sizeof(float) * sv->ncells,
+                              cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaMemcpyAsync(sv->d_flags, flags, sv->ncells, cudaMemcpyHostToDevice, s));
+    if (counts)
+      DARE_CUDA(cudaMemcpyAsync(sv->d_counts, counts, sizeof(int64_t) * sv->ncells,
+                                cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaStreamSynchronize(s));
+    *out = sv.release();
+  });
+}
+
+extern "C" int dare_scalar_download(dare_scalar_t vol, float* values, uint8_t* flags,
+                                    int64_t* counts) {
+  return guard([&] {
+    DARE_REQUIRE(vol != nullptr, "null volume");
+    cudaStream_t s = thread_stream();
+    if (values)
+      DARE_CUDA(cudaMemcpyAsync(values, vol->d_values, sizeof(float) * vol->ncells,
+                                cudaMemcpyDeviceToHost, s));
+    if (flags) DARE_CUDA(cudaMemcpyAsync(flags, vol->d_flags, vol->ncells, cudaMemcpyDeviceToHost, s));
+    if (counts && vol->d_counts)
+      DARE_CUDA(cudaMemcpyAsync(counts, vol->d_counts, sizeof(int64_t) * vol->ncells,
+                                cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int dare_scalar_get_info(dare_scalar_t vol, dare_scalar_info* info) {
+  return guard([&] {
+    DARE_REQUIRE(vol != nullptr && info != nullptr, "null argument");
+    info->device = vol->device;
+    for (int a = 0; a < 3; ++a) {
+      info->origin[a] = vol->origin[a];
+      info->dims[a] = vol->dims[a];
+    }
+    info->voxel_size = vol->voxel;
+    info->d_values = vol->d_values;
+    info->d_flags = vol->d_flags;
+    info->d_counts = vol->d_counts;
+  });
+}
+
+extern "C" int dare_scalar_destroy(dare_scalar_t vol) {
+  return guard([&] { delete vol; });
+}
+
+extern "C" int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar_t* out,
+                               int32_t* passes_run) {
+  return guard([&] {
+    DARE_REQUIRE(in != nullptr && out != nullptr, "null argument");
+    DARE_REQUIRE(max_passes >= 0 && max_passes <= 250, "max_passes must be in [0, 250]");
+    cudaStream_t s = thread_stream();
+    auto sv = new_scalar(in->origin, in->voxel, in->dims, in->d_counts != nullptr);
+    const int64_t n = in->ncells;
+    Scratch<double> work(n, s);
+    Scratch<uint8_t> flags(n, s);
+    Scratch<unsigned long long> filled(std::max(max_passes, 1), s);
+    DARE_CUDA(cudaMemsetAsync(filled.ptr, 0, sizeof(unsigned long long) * std::max(max_passes, 1), s));
+    DARE_CUDA(cudaMemcpyAsync(flags.ptr, in->d_flags, n, cudaMemcpyDeviceToDevice, s));
+    to_f64_k<<<ceil_div(n, 256), 256, 0, s>>>(n, in->d_values, work.ptr);
+    for (int p = 0; p < max_passes; ++p) {
+      fill_pass_k<<<ceil_div(n, 256), 256, 0, s>>>(in->dims[0], in->dims[1], in->dims[2],
+                                                    work.ptr, flags.ptr, 3 + p, filled.ptr + p,
+                                                    p ? filled.ptr + p - 1 : nullptr);
+      DARE_CUDA(cudaGetLastError());
+    }
+    fill_finalize_k<<<ceil_div(n, 256), 256, 0, s>>>(n, work.ptr, flags.ptr, sv->d_values,
+                                                     sv->d_flags);
+    DARE_CUDA(cudaGetLastError());
+    if (in->d_counts)
+      DARE_CUDA(cudaMemcpyAsync(sv->d_counts, in->d_counts, sizeof(int64_t) * n,
+                                cudaMemcpyDeviceToDevice, s));
+    std::vector<unsigned long long> h(std::max(max_passes, 1));
+    DARE_CUDA(cudaMemcpyAsync(h.data(), filled.ptr, sizeof(unsigned long long) * h.size(),
+                              cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaStreamSynchronize(s));
+    int32_t runs = 0;
+    for (int p = 0; p < max_passes; ++p) runs += h[p] > 0;
+    if (passes_run) *passes_run = runs;
+    *out = sv.release();
+  });
+}
+
+extern "C" int dare_reslice_trilinear_device(dare_scalar_t vol, int32_t n_poses,
+                                             const double* d_params, int32_t width,
+                                             int32_t height, uint8_t* d_pixels,
+                                             uint8_t* d_coverage, double* d_values,
+                                             void* stream) {
+  return guard([&] {
+    cudaStream_t s = stream ? (cudaStream_t)stream : thread_stream();
+    launch_trilinear(vol, n_poses, d_params, width, height, d_pixels, d_coverage, d_values, s);
+  });
+}
+
+extern "C" int dare_reslice_trilinear(dare_scalar_t vol, int32_t n_poses, const double* params,
+                                      int32_t width, int32_t height, uint8_t* pixels,
+                                      uint8_t* coverage, double* values) {
+  return guard([&] {
+    DARE_REQUIRE(n_poses >= 0, "negative pose count");
+    if (n_poses == 0) return;
+    cudaStream_t s = thread_stream();
+    const size_t npix = (size_t)n_poses * width * height;
+    Scratch<double> d_params((size_t)n_poses * 14, s);
+    Scratch<uint8_t> d_out(2 * npix, s);
+    Scratch<double> d_val(values ? npix : 0, s);
+    DARE_CUDA(cudaMemcpyAsync(d_params.ptr, params, sizeof(double) * 14 * n_poses,
+                              cudaMemcpyHostToDevice, s));
+    for (int32_t p0 = 0; p0 < n_poses; p0 += 65535) {
+      int32_t np = std::min<int32_t>(65535, n_poses - p0);
+      size_t off = (size_t)p0 * width * height;
+      launch_trilinear(vol, np, d_params.ptr + (size_t)p0 * 14, width, height, d_out.ptr + off,
+                       d_out.ptr + npix + off, values ? d_val.ptr + off : nullptr, s);
+    }
+    DARE_CUDA(cudaMemcpyAsync(pixels, d_out.ptr, npix, cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaMemcpyAsync(coverage, d_out.ptr + npix, npix, cudaMemcpyDeviceToHost, s));
+    if (values)
+      DARE_CUDA(cudaMemcpyAsync(values, d_val.ptr, sizeof(double) * npix, cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaStreamSynchronize(s));
+  });
+}

@@ -1,0 +1,268 @@
+"""Parity of the CUDA path (through the C ABI) with the reference golden
+outputs and with the CPU oracle.  Bit-exact for indices, counts, positions,
+orientations, intensities, pixels and coverage (no tolerance is needed: the
+device restates the reference's f64 operation order and glibc's exp)."""
+import math
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import paper_2605_26325_b200 as db
+from golden_io import REC_KEYS, SEAL_KEYS
+from oracle import oracle
+from paper_2605_26325_b200 import _lib
+from paper_2605_26325_b200.geometry import Pose, Quaternion
+from paper_2605_26325_b200.reslice import ReslicePlane, ResliceConfig
+
+pytestmark = pytest.mark.gpu
+
+FILL_ORIGIN = (0.5, -1.0, 2.0)
+FILL_VOXEL = 0.5
+VOL_FIELDS = ("cell_starts", "cell_counts", "positions", "orientations", "intensities")
+
+
+def assert_volume_equal(v, ref):
+    np.testing.assert_array_equal(v.origin, ref.origin)
+    assert tuple(v.dims) == tuple(ref.dims)
+    for name in VOL_FIELDS:
+        np.testing.assert_array_equal(getattr(v, name), getattr(ref, name), err_msg=name)
+    assert v.rejected_out_of_bounds == ref.rejected_out_of_bounds
+
+
+def test_device_present():
+    assert _lib.device_count() >= 1
+
+
+def test_exp_device_bit_exact(golden, rng):
+    import torch
+
+    x = np.concatenate([golden["exp.x"], -rng.uniform(0, 60, 2_000_000), rng.uniform(-1100, 1100, 100_000)])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.call("dare_exp_device", _lib.c_vp(xd.data_ptr()), _lib.c_vp(yd.data_ptr()), len(x), _lib.c_vp(0))
+    _lib.call("dare_stream_sync", _lib.c_vp(0))
+    y = yd.cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint64), oracle.exp(x).view(np.uint64))
+
+
+@pytest.mark.parametrize("key", REC_KEYS)
+def test_reconstruct_matches_reference(golden, key):
+    rec, voxel, margin = golden.sweep(key)
+    v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
+    assert_volume_equal(v, golden.volume(key + ".out"))
+
+
+def _random_sweep(rng, n, h, w, pitch, spread):
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    poses = [Pose(Quaternion(*qq), rng.uniform(-spread, spread, 3)) for qq in q]
+    ts = np.arange(n) * 0.03
+    return db.SweepRecording(rng.integers(0, 256, (n, h, w), dtype=np.uint8), ts, ts, poses, pitch)
+
+
+@pytest.mark.parametrize("seed,voxel,margin", [(1, 0.25, 0.0), (2, 0.1, 0.5), (3, 0.37, 1.0)])
+def test_reconstruct_random_sweeps_match_oracle(seed, voxel, margin):
+    rng = np.random.default_rng(seed)
+    rec = _random_sweep(rng, 40, 33, 47, (0.11, 0.09), 2.0)
+    v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
+    assert_volume_equal(v, oracle.reconstruct(rec, voxel, margin))
+
+
+def test_reconstruct_dense_cells_use_large_run_path():
+    # many frames at one pose: > 32 samples per cell -> segmented-sort path
+    rng = np.random.default_rng(5)
+    n = 80
+    ts = np.arange(n) * 0.1
+    rec = db.SweepRecording(rng.integers(0, 256, (n, 6, 5), dtype=np.uint8), ts, ts, [Pose.identity()] * n,
+                            (0.05, 0.05))
+    v = db.reconstruct_volume(rec, voxel_size=0.5, margin=0.25)
+    assert v.cell_counts.max() > 32
+    assert_volume_equal(v, oracle.reconstruct(rec, 0.5, 0.25))
+
+
+@pytest.mark.parametrize("key", SEAL_KEYS)
+def test_volume_builder_seal_matches_reference(golden, key):
+    b = golden[f"{key}.bounds"]
+    builder = db.VolumeBuilder(db.BoundingBox(b[:3], b[3:]), float(golden[f"{key}.voxel"]))
+    builder.insert_batch(golden[f"{key}.in_pos"], golden[f"{key}.in_quat"], golden[f"{key}.in_inten"])
+    v = builder.seal()
+    v.rejected_out_of_bounds = builder.rejected_out_of_bounds
+    assert_volume_equal(v, golden.volume(key + ".out"))
+
+
+def test_reslice_matches_reference_goldens(golden):
+    vols = {}
+    for i, c in golden.reslice_cases():
+        if c.vol_key not in vols:
+            vols[c.vol_key] = golden.full_volume(c.vol_key)  # foreign (reference-layout) volume
+        vol = vols[c.vol_key]
+        out = db.reslice(vol, c.plane, c.cfg)
+        np.testing.assert_array_equal(out.pixels, c.pixels, err_msg=f"rs_{i}")
+        np.testing.assert_array_equal(out.coverage, c.coverage, err_msg=f"rs_{i}")
+        if c.brute is not None:
+            b = db.reslice_bruteforce(vol, c.plane, c.cfg)
+            np.testing.assert_array_equal(b.pixels, c.brute[0])
+            np.testing.assert_array_equal(b.coverage, c.brute[1])
+
+
+def _random_volume(rng, n, extent=10.0, voxel=0.5):
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (extent,) * 3), voxel)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[q[:, 0] < 0] *= -1.0
+    b.insert_batch(rng.uniform(0, extent, (n, 3)), q, rng.integers(0, 256, n))
+    return b.seal()
+
+
+def test_acceptance_criterion_1_against_oracle(rng):
+    """>= 100 randomized (volume, plane, config) cases, bit-exact vs the CPU oracle
+    (grid and brute force), as test_acceptance.py:92-123 does for the reference."""
+    for case in range(100):
+        vol = _random_volume(rng, int(rng.integers(0, 10_001)), 10.0, float(rng.choice([0.25, 0.5, 1.0])))
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        plane = ReslicePlane(Pose(Quaternion(*q), rng.uniform(-1, 11, 3)), int(rng.integers(4, 25)),
+                             int(rng.integers(4, 25)), (float(rng.uniform(0.1, 0.6)),) * 2)
+        cfg = ResliceConfig(interp_radius=float(rng.uniform(0.15, 1.5)),
+                            normal_threshold_deg=float(rng.uniform(5, 85)),
+                            inplane_threshold_deg=float(rng.uniform(5, 85)), k_normal=float(rng.uniform(0, 20)),
+                            k_inplane=float(rng.uniform(0, 10)), k_dist=float(rng.choice([0.0, 1.0, 2.0, 4.0])),
+                            unassigned_value=int(rng.integers(0, 256)))
+        fast = db.reslice(vol, plane, cfg)
+        ref = oracle.reslice(vol, oracle.plane_params(plane), oracle.cfg_array(cfg), plane.width, plane.height,
+                             cfg.unassigned_value)
+        np.testing.assert_array_equal(fast.pixels, ref[0], err_msg=f"case {case}")
+        np.testing.assert_array_equal(fast.coverage, ref[1], err_msg=f"case {case}")
+        brute = db.reslice_bruteforce(vol, plane, cfg)
+        np.testing.assert_array_equal(brute.pixels, fast.pixels)
+        np.testing.assert_array_equal(brute.coverage, fast.coverage)
+
+
+def test_reslice_batch_equals_single_calls(rng):
+    vol = _random_volume(rng, 20000, 10.0, 0.25)
+    planes = []
+    for _ in range(9):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        planes.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(2, 8, 3)), 40, 33, (0.2, 0.2)))
+    cfg = ResliceConfig(interp_radius=0.25)
+    px, cov, _ = db.reslice_batch(vol, planes, cfg)
+    for k, p in enumerate(planes):
+        one = db.reslice(vol, p, cfg)
+        np.testing.assert_array_equal(px[k], one.pixels)
+        np.testing.assert_array_equal(cov[k], one.coverage)
+
+
+def test_concurrent_reslices_identical(rng):
+    vol = _random_volume(rng, 4000)
+    plane = ReslicePlane(Pose(Quaternion.identity(), (2.0, 2.0, 5.0)), 24, 20, (0.3, 0.3))
+    cfg = ResliceConfig(interp_radius=0.6, normal_threshold_deg=80, inplane_threshold_deg=80)
+    ref = db.reslice(vol, plane, cfg)
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        results = list(pool.map(lambda _: db.reslice(vol, plane, cfg), range(24)))
+    for r in results:
+        np.testing.assert_array_equal(r.pixels, ref.pixels)
+        np.testing.assert_array_equal(r.coverage, ref.coverage)
+
+
+def test_reference_behaviour_cases():
+    # empty volume -> all unassigned (test_reslice.py:164-169)
+    vol = _random_volume(np.random.default_rng(0), 0)
+    out = db.reslice(vol, ReslicePlane(Pose.identity(), 5, 4, (0.3, 0.3)), ResliceConfig(unassigned_value=7))
+    assert not out.coverage.any() and (out.pixels == 7).all()
+    # single sample (test_reslice.py:171-179)
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (4, 4, 1)), 0.25)
+    b.insert_sample(db.DirectionalSample(177, Quaternion.identity(), (2.0, 2.0, 0.5)))
+    vol = b.seal()
+    plane = ReslicePlane(Pose(Quaternion.identity(), (2.0, 2.0, 0.5)), 1, 1, (0.25, 0.25))
+    for fn in (db.reslice, db.reslice_bruteforce):
+        o = fn(vol, plane, ResliceConfig(interp_radius=0.25))
+        assert o.coverage[0, 0] and o.pixels[0, 0] == 177
+    # cube, not ball (test_reslice.py:247-257)
+    r = 0.25
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (4, 4, 2)), r)
+    b.insert_sample(db.DirectionalSample(99, Quaternion.identity(), np.array([2.0 + r, 2.0 + r, 0.5 + r]) - 1e-6))
+    o = db.reslice(b.seal(), ReslicePlane(Pose(Quaternion.identity(), (2.0, 2.0, 0.5)), 1, 1, (r, r)),
+                   ResliceConfig(interp_radius=r))
+    assert o.coverage[0, 0]
+    # 25 degree gate rejects a 30 degree tilt, 40 accepts (test_reslice.py:232-240)
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (4, 4, 1)), 0.25)
+    b.insert_sample(db.DirectionalSample(200, Quaternion.from_axis_angle((1, 0, 0), math.radians(30)),
+                                         (2.0, 2.0, 0.5)))
+    vol = b.seal()
+    assert not db.reslice(vol, plane, ResliceConfig(interp_radius=0.25)).coverage[0, 0]
+    assert db.reslice(vol, plane, ResliceConfig(interp_radius=0.25, normal_threshold_deg=40)).coverage[0, 0]
+
+
+def test_single_frame_round_trip_within_one_gray(rng):
+    """Acceptance criterion 2 (test_acceptance.py:126-139)."""
+    img = rng.integers(0, 256, (48, 64), dtype=np.uint8)
+    rec = db.SweepRecording(img[None], [0.0], [0.0], [Pose.identity()], (0.2, 0.2))
+    vol = db.reconstruct_volume(rec, voxel_size=0.125, margin=0.5)
+    out = db.reslice(vol, ReslicePlane(Pose.identity(), 64, 48, (0.2, 0.2)), ResliceConfig())
+    assert out.coverage.all()
+    assert np.abs(out.pixels.astype(int) - img.astype(int)).max() <= 1
+
+
+@pytest.mark.parametrize("key", ("rec_tilt", "rec_mask", "rec_parallel", "rec_margin0"))
+def test_compound_matches_reference(golden, key):
+    rec, voxel, margin = golden.sweep(key)
+    s = db.compound(rec, voxel_size=voxel, margin=margin)
+    np.testing.assert_array_equal(s.origin, golden[f"cmp_{key}.origin"])
+    np.testing.assert_array_equal(s.values, golden[f"cmp_{key}.values"])
+    np.testing.assert_array_equal(s.flags, golden[f"cmp_{key}.flags"])
+    np.testing.assert_array_equal(s.counts, golden[f"cmp_{key}.counts"])
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_fill_holes_and_trilinear_match_reference(golden, i):
+    dims = tuple(int(d) for d in golden[f"fill_{i}.dims"])
+    sv = db.ScalarVolume(FILL_ORIGIN, FILL_VOXEL, dims, golden[f"fill_{i}.in_values"], golden[f"fill_{i}.in_flags"])
+    out = db.fill_holes(sv, max_passes=int(golden[f"fill_{i}.passes"]))
+    np.testing.assert_array_equal(out.values, golden[f"fill_{i}.values"])
+    np.testing.assert_array_equal(out.flags, golden[f"fill_{i}.flags"])
+    for j in range(3):
+        key = f"tri_{i}_{j}"
+        r = db.reslice_trilinear(out, golden.trilinear_plane(key))
+        np.testing.assert_array_equal(r.pixels, golden[f"{key}.pixels"])
+        np.testing.assert_array_equal(r.coverage, golden[f"{key}.coverage"])
+
+
+def test_scalar_arm_random_sweep_matches_oracle():
+    rng = np.random.default_rng(11)
+    rec = _random_sweep(rng, 30, 21, 25, (0.1, 0.1), 1.5)
+    s = db.compound(rec, voxel_size=0.2, margin=0.3)
+    origin, voxel, dims, values, flags, counts = oracle.compound(rec, 0.2, 0.3)
+    np.testing.assert_array_equal(s.values, values)
+    np.testing.assert_array_equal(s.counts, counts)
+    f = db.fill_holes(s, 3)
+    fv, ff = oracle.fill_holes(values, flags, dims, 3)
+    np.testing.assert_array_equal(f.values, fv)
+    np.testing.assert_array_equal(f.flags, ff)
+    for k in range(5):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        plane = ReslicePlane(Pose(Quaternion(*q), rng.uniform(-1, 1, 3)), 31, 29, (0.07, 0.07))
+        r = db.reslice_trilinear(f, plane)
+        px, cov, _ = oracle.trilinear(origin, voxel, dims, fv, ff, oracle.plane_params(plane), 31, 29)
+        np.testing.assert_array_equal(r.pixels, px)
+        np.testing.assert_array_equal(r.coverage, cov)
+
+
+def test_trilinear_at_points_values():
+    vals = np.zeros((2, 1, 1), np.float32)
+    vals[1, 0, 0] = 200.0
+    sv = db.ScalarVolume((0, 0, 0), 1.0, (2, 1, 1), vals.reshape(-1), np.ones(2, np.uint8))
+    v, c = db.trilinear_at_points(sv, [(1.0, 0.5, 0.5)])
+    assert c[0] and v[0] == 100.0
+
+
+def test_darevol_from_device_volume_identical(golden, tmp_path):
+    import hashlib
+
+    rec, voxel, margin = golden.sweep("rec_tilt")
+    v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
+    path = tmp_path / "v.darevol"
+    db.save_volume(v, path)
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == str(golden["rec_tilt.darevol_sha256"])
