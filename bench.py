@@ -116,7 +116,7 @@ class DevArray:
     """__cuda_array_interface__ view of a raw device pointer (for torch.as_tensor)."""
 
     def __init__(self, ptr: int, shape, typestr: str):
-        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), True),
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
                                          "version": 2}
 
 
@@ -319,7 +319,9 @@ def run_b200(args):
     H = W = wl.plane
     out_d = torch.empty((2, B, H, W), dtype=torch.uint8, device="cuda")
     kc = kernel_cfg(cfg)
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream: the kernels and the timing events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = ctypes.c_void_p(stream.cuda_stream)
     handle = vol.device_handle().raw
 

@@ -79,6 +79,27 @@ struct Scratch {
 
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
+// Development aid: with DARE_PROFILE=1 in the environment, records CUDA events
+// at phase boundaries on `stream` and prints per-phase device times to stderr
+// when it goes out of scope.  No cost when disabled.
+class PhaseTimer {
+ public:
+  PhaseTimer(cudaStream_t s, const char* what);
+  ~PhaseTimer();
+  void mark(const char* phase);
+
+ private:
+  bool on_ = false;
+  cudaStream_t s_ = nullptr;
+  const char* what_ = nullptr;
+  struct Mark {
+    const char* name;
+    cudaEvent_t ev;
+  };
+  Mark marks_[32];
+  int n_ = 0;
+};
+
 // True when 1/x is exactly representable, so (y / x) == (y * (1/x)) bit-for-bit
 // (both are the correctly rounded value of the same real number).
 inline bool exact_reciprocal(double x) {
@@ -89,6 +110,16 @@ inline bool exact_reciprocal(double x) {
 }
 
 int sm_count();
+
+// Long-lived device buffers (volumes) come from the device's stream-ordered
+// pool with an unlimited release threshold, so rebuilding a volume reuses
+// memory instead of paying cudaMalloc/cudaFree of multi-GB buffers.
+void dev_alloc_bytes(void** p, size_t bytes);
+void dev_free(void* p);
+template <class T>
+inline void dev_alloc(T** p, size_t bytes) {
+  dev_alloc_bytes((void**)p, bytes);
+}
 
 }  // namespace dare
 

@@ -33,11 +33,12 @@ struct FrameView {
   int64_t n_frames;
   int32_t H, W;
   double px, py;
+  const uint32_t* oid;  // orientation id per synchronized frame
 };
 
 static FrameView view_of(const FrameSet& fs) {
   return FrameView{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
-                   fs.H,        fs.W,       fs.px,     fs.py};
+                   fs.H,        fs.W,       fs.px,     fs.py,      nullptr};
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -140,7 +141,7 @@ struct FrameRecords {
       p32[a] = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
     uint8_t inten = fv.frames[(size_t)fv.image[f] * hw + p];
     return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
-                      (f << 8) | inten);
+                      (fv.oid[f] << 8) | inten);
   }
 };
 
@@ -205,13 +206,16 @@ __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_
 template <class Rec, class Scatter>
 void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   const int64_t ncells = vol->ncells;
+  PhaseTimer pt(s, "build_csr");
   Scratch<uint32_t> counts(ncells + 1, s);
   Scratch<unsigned long long> rej(1, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (ncells + 1), s));
   DARE_CUDA(cudaMemsetAsync(rej.ptr, 0, sizeof(unsigned long long), s));
-  DARE_CUDA(cudaMalloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1)));
+  dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
+  pt.mark("alloc+memset");
   scatter(false, counts.ptr, (const uint32_t*)nullptr, (uint32_t*)nullptr, rej.ptr);
   DARE_CUDA(cudaGetLastError());
+  pt.mark("count");
   size_t tmp_bytes = 0;
   DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.ptr, vol->d_offsets,
                                           ncells + 1, s));
@@ -220,6 +224,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
     DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, counts.ptr, vol->d_offsets,
                                             ncells + 1, s));
   }
+  pt.mark("scan");
   uint32_t n_kept = 0;
   unsigned long long n_rej = 0;
   DARE_CUDA(cudaMemcpyAsync(&n_kept, vol->d_offsets + ncells, sizeof(uint32_t),
@@ -228,19 +233,22 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   DARE_CUDA(cudaStreamSynchronize(s));
   vol->n_samples = n_kept;
   vol->rejected = (int64_t)n_rej;
-  DARE_CUDA(cudaMalloc(&vol->d_records, sizeof(uint4) * std::max<uint32_t>(n_kept, 1)));
+  dev_alloc(&vol->d_records, sizeof(uint4) * std::max<uint32_t>(n_kept, 1));
   if (n_kept == 0) return;
   Scratch<uint32_t> keys(n_kept, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncells, s));
+  pt.mark("readback+alloc");
   scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, keys.ptr,
           (unsigned long long*)nullptr);
   DARE_CUDA(cudaGetLastError());
+  pt.mark("fill");
   uint32_t* big_cells = counts.ptr;  // reuse: #big runs <= ncells
   Scratch<uint32_t> n_big_d(1, s);
   DARE_CUDA(cudaMemsetAsync(n_big_d.ptr, 0, sizeof(uint32_t), s));
   seal_k<<<ceil_div(ncells, 256), 256, 0, s>>>(rec, vol->d_offsets, keys.ptr, ncells,
                                                 vol->d_records, big_cells, n_big_d.ptr);
   DARE_CUDA(cudaGetLastError());
+  pt.mark("seal");
   uint32_t n_big = 0;
   DARE_CUDA(cudaMemcpyAsync(&n_big, n_big_d.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
@@ -297,10 +305,21 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                 frame_axes, pitch_x, pitch_y, mask, s);
     FrameView fv = view_of(fs);
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
-    vol->n_orient = n_frames;
-    if (n_frames > 0) {
-      DARE_CUDA(cudaMalloc(&vol->d_orient, sizeof(float4) * n_frames));
-      DARE_CUDA(cudaMemcpyAsync(vol->d_orient, frame_quats, sizeof(float4) * n_frames,
+    // frames sharing a canonical f32 quaternion share an orientation id, so the
+    // reslice gate table stays tiny for sweeps with few distinct orientations
+    std::vector<uint32_t> word((size_t)std::max<int64_t>(n_frames, 1));
+    std::vector<uint8_t> zeros((size_t)std::max<int64_t>(n_frames, 1), 0);
+    std::vector<float4> table;
+    dedup_orientations(frame_quats, zeros.data(), n_frames, word.data(), table);
+    for (auto& w : word) w >>= 8;
+    Scratch<uint32_t> d_oid((size_t)std::max<int64_t>(n_frames, 1), s);
+    DARE_CUDA(cudaMemcpyAsync(d_oid.ptr, word.data(), sizeof(uint32_t) * word.size(),
+                              cudaMemcpyHostToDevice, s));
+    fv.oid = d_oid.ptr;
+    vol->n_orient = (int64_t)table.size();
+    if (!table.empty()) {
+      dev_alloc(&vol->d_orient, sizeof(float4) * table.size());
+      DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
                                 cudaMemcpyHostToDevice, s));
     }
     dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(std::max<int64_t>(n_frames, 1), 65535));
@@ -336,7 +355,7 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
     dedup_orientations(orientations, intensities, n_samples, word.data(), table);
     cudaStream_t s = thread_stream();
     vol->n_orient = (int64_t)table.size();
-    DARE_CUDA(cudaMalloc(&vol->d_orient, sizeof(float4) * std::max<size_t>(table.size(), 1)));
+    dev_alloc(&vol->d_orient, sizeof(float4) * std::max<size_t>(table.size(), 1));
     if (!table.empty())
       DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
                                 cudaMemcpyHostToDevice, s));

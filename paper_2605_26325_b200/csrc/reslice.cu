@@ -22,6 +22,8 @@
 #include <math_constants.h>
 
 #include "dare_exp.h"
+#include <cub/device/device_radix_sort.cuh>
+
 #include "volume.cuh"
 
 namespace dare {
@@ -44,6 +46,7 @@ struct ResliceArgs {
   int W, H, P;
   int tiles_x;
   int brute;           // 1: scan every sample (reslice_rows_bruteforce)
+  const int* order;    // launch slot -> pose (spatially sorted batch), or null
   uint32_t n_samples;
 };
 
@@ -87,66 +90,148 @@ __device__ __forceinline__ void cell_range(double w, double r, double o, double 
   hi = h >= (double)n ? n - 1 : (h < -1.0 ? -1 : (int64_t)h);
 }
 
-// 256 threads = one 16x16 pixel tile; each warp covers 8x4 pixels.
+// Exact f32 form of the reference's closed cube test on one axis:
+// keep  <=>  -r <= fl64(f64(p) - w) <= r.  fl64(p - w) is monotone in p, so the
+// kept f32 values form an interval [lo, hi]; find its ends by stepping ulps
+// from the rounded guesses (<= 2 steps in practice).
+__device__ __forceinline__ float keep_hi(double w, double r) {
+  float p = __double2float_rn(w + r);
+  for (int i = 0; i < 4 && !((double)p - w <= r); ++i) p = nextafterf(p, -CUDART_INF_F);
+  for (int i = 0; i < 4; ++i) {
+    float q = nextafterf(p, CUDART_INF_F);
+    if ((double)q - w <= r) p = q;
+    else break;
+  }
+  return p;
+}
+
+__device__ __forceinline__ float keep_lo(double w, double r) {
+  float p = __double2float_rn(w - r);
+  for (int i = 0; i < 4 && !((double)p - w >= -r); ++i) p = nextafterf(p, CUDART_INF_F);
+  for (int i = 0; i < 4; ++i) {
+    float q = nextafterf(p, -CUDART_INF_F);
+    if ((double)q - w >= -r) p = q;
+    else break;
+  }
+  return p;
+}
+
+constexpr int kGateSmem = 512;  // orientation table entries staged in shared memory
+constexpr int kSmemBytes = (int)(sizeof(double) * kGateSmem);
+
+// 256 threads = one 16x16 pixel tile; each warp covers 8x4 pixels; thread per
+// pixel, walking its cell columns in the reference order.  Per-visit work is
+// an exact f32 interval test (keep_lo/keep_hi) plus, when this pose rejects
+// any orientation, the gate lookup; survivors get the FP64 weight.  To keep
+// the FP64 path converged, the warp advances in rounds: every lane scans
+// forward to its next survivor (cheap, divergent), then all lanes that found
+// one evaluate it together.
+//
+// Measured alternatives (profiles/round1_reslice_variants.md): warp-
+// cooperative run scans with per-pixel survivor rows (coalesced, DRAM at the
+// compulsory 59 MB/pose) and per-lane survivor queues both lost to this
+// version on instruction count or on L1 capacity.
+template <int kDistMode>
 __global__ void __launch_bounds__(256) reslice_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                  uint8_t* __restrict__ cov) {
-  const int pose = blockIdx.y;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_gate = reinterpret_cast<double*>(smem_raw);
+  const int pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+  const double* __restrict__ gate_g = a.gate + (size_t)pose * a.n_orient;
+  const bool gate_in_smem = a.n_orient <= kGateSmem;
+  bool gate_filter = true;  // some orientation rejected for this pose -> test it per visit
+  if (gate_in_smem) {
+    bool rej = false;
+    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
+      const double g = gate_g[i];
+      s_gate[i] = g;
+      rej |= g == CUDART_INF;
+    }
+    gate_filter = __syncthreads_or(rej);
+  }
+  const double* gate = gate_in_smem ? s_gate : gate_g;
+
   const int tile = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = (tile % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
   const int v = (tile / a.tiles_x) * 16 + (warp >> 1) * 4 + (lane >> 3);
-  if (u >= a.W || v >= a.H) return;
+  const bool active = u < a.W && v < a.H;
 
   const double* pp = a.params + (size_t)pose * 14;
-  const double tx = pp[0], ty = pp[1], tz = pp[2];
-  const double r00 = pp[3], r01 = pp[4], r10 = pp[6], r11 = pp[7], r20 = pp[9], r21 = pp[10];
-  const double pitch_x = pp[12], pitch_y = pp[13];
-  const double du = (double)u * pitch_x, dv = (double)v * pitch_y;
-  const double wx = (tx + du * r00) + dv * r01;
-  const double wy = (ty + du * r10) + dv * r11;
-  const double wz = (tz + du * r20) + dv * r21;
+  const double du = (double)u * pp[12], dv = (double)v * pp[13];
+  const double wx = (pp[0] + du * pp[3]) + dv * pp[4];
+  const double wy = (pp[1] + du * pp[6]) + dv * pp[7];
+  const double wz = (pp[2] + du * pp[9]) + dv * pp[10];
   const double r = a.radius;
   const double inv_v = 1.0 / a.voxel;
   int64_t lox, hix, loy, hiy, loz, hiz;
   cell_range(wx, r, a.origin[0], inv_v, a.dims[0], lox, hix);
   cell_range(wy, r, a.origin[1], inv_v, a.dims[1], loy, hiy);
   cell_range(wz, r, a.origin[2], inv_v, a.dims[2], loz, hiz);
+  const float xlo = keep_lo(wx, r), xhi = keep_hi(wx, r);
+  const float ylo = keep_lo(wy, r), yhi = keep_hi(wy, r);
+  const float zlo = keep_lo(wz, r), zhi = keep_hi(wz, r);
 
-  const double* __restrict__ gate = a.gate + (size_t)pose * a.n_orient;
+  // run cursor over the (cx, cy) columns; each column's cells loz..hiz are one
+  // contiguous sample range [off[base+loz], off[base+hiz+1])
+  int64_t cx = lox, cy = loy;
+  uint32_t s = 0, e = 0;
+  auto open_run = [&]() -> bool {
+    if (a.brute) {
+      if (cx > lox) return false;
+      s = 0;
+      e = a.n_samples;
+      cx = lox + 1;
+      return s < e;
+    }
+    while (cx <= hix) {
+      const int64_t base = (cx * a.dims[1] + cy) * a.dims[2];
+      s = __ldg(a.offsets + base + loz);
+      e = __ldg(a.offsets + base + hiz + 1);
+      if (++cy > hiy) {
+        cy = loy;
+        ++cx;
+      }
+      if (s < e) return true;
+    }
+    return false;
+  };
+  bool live = active && (a.brute ? true : (lox <= hix && loy <= hiy && loz <= hiz)) && open_run();
+  uint4 nxt = make_uint4(0, 0, 0, 0);
+  if (live) nxt = __ldg(a.records + s);
+
   double wsum = 0.0, iwsum = 0.0;
-  // _accumulate_run over samples [s0, s1) in storage order
-  auto run = [&](uint32_t s0, uint32_t s1) {
-    for (uint32_t s = s0; s < s1; ++s) {
-      const uint4 rec = __ldg(a.records + s);
-      const double A = __ldg(gate + (rec.w >> 8));
-      if (A == CUDART_INF) continue;
-      const double dx = (double)__uint_as_float(rec.x) - wx;
-      if (dx < -r || dx > r) continue;
-      const double dy = (double)__uint_as_float(rec.y) - wy;
-      if (dy < -r || dy > r) continue;
-      const double dz = (double)__uint_as_float(rec.z) - wz;
-      if (dz < -r || dz > r) continue;
-      double arg = A;
-      if (a.dist_mode != 2) {
+  while (true) {
+    bool found = false;
+    uint4 cur;
+    while (live) {
+      cur = nxt;
+      if (++s == e) live = open_run();
+      if (live) nxt = __ldg(a.records + s);  // prefetch the next visit
+      const float x = __uint_as_float(cur.x), y = __uint_as_float(cur.y), z = __uint_as_float(cur.z);
+      if (x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi &&
+          (!gate_filter || gate[cur.w >> 8] != CUDART_INF)) {
+        found = true;
+        break;
+      }
+    }
+    if (!__any_sync(0xffffffffu, found)) break;
+    if (found) {
+      const double dx = (double)__uint_as_float(cur.x) - wx;
+      const double dy = (double)__uint_as_float(cur.y) - wy;
+      const double dz = (double)__uint_as_float(cur.z) - wz;
+      double arg = gate[cur.w >> 8];
+      if (kDistMode != 2) {
         const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
         const double kdd = a.kd * dist;
-        arg = A - (a.dist_mode == 1 ? kdd * a.inv_radius : kdd / r);
+        arg = arg - (kDistMode == 1 ? kdd * a.inv_radius : kdd / r);
       }
       const double w = dare_exp(arg);
       wsum += w;
-      iwsum += w * (double)(rec.w & 0xffu);
-    }
-  };
-  if (a.brute) {
-    run(0, a.n_samples);  // reslice_rows_bruteforce (_kernels.py:142-167)
-  } else if (loz <= hiz) {
-    for (int64_t cx = lox; cx <= hix; ++cx) {
-      for (int64_t cy = loy; cy <= hiy; ++cy) {
-        const int64_t base = (cx * a.dims[1] + cy) * a.dims[2];
-        run(__ldg(a.offsets + base + loz), __ldg(a.offsets + base + hiz + 1));
-      }
+      iwsum += w * (double)(cur.w & 0xffu);
     }
   }
+  if (!active) return;
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
   if (wsum >= kCoverageMinWeight) {
     double f = floor(iwsum / wsum + 0.5);
@@ -157,6 +242,29 @@ __global__ void __launch_bounds__(256) reslice_k(ResliceArgs a, uint8_t* __restr
     out[k] = (uint8_t)a.unassigned;
     cov[k] = 0;
   }
+}
+
+// Batch scheduling: blocks are dispatched pose-major, so ~2 poses are in flight
+// at a time.  Launching the batch in spatial order (plane centre, coarse z
+// then y then x) makes consecutive poses share cells in L2.  Pure
+// scheduling: every pose's pixels are computed exactly as before.
+__global__ void pose_key_k(const double* __restrict__ params, int P, int W, int H, double ox,
+                           double oy, double oz, double cell, unsigned long long* keys, int* idx) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double* pp = params + (size_t)p * 14;
+  const double hu = 0.5 * (W - 1) * pp[12], hv = 0.5 * (H - 1) * pp[13];
+  const double c[3] = {pp[0] + hu * pp[3] + hv * pp[4], pp[1] + hu * pp[6] + hv * pp[7],
+                       pp[2] + hu * pp[9] + hv * pp[10]};
+  const double o[3] = {ox, oy, oz};
+  unsigned long long q[3];
+  for (int k = 0; k < 3; ++k) {
+    double f = floor((c[k] - o[k]) / cell);
+    f = f < 0.0 ? 0.0 : (f > 1048575.0 ? 1048575.0 : (f != f ? 0.0 : f));
+    q[k] = (unsigned long long)f;
+  }
+  keys[p] = (q[2] << 40) | (q[1] << 20) | q[0];
+  idx[p] = p;
 }
 
 __global__ void exp_k(const double* x, double* y, int64_t n) {
@@ -194,6 +302,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.brute = brute;
   a.n_samples = (uint32_t)vol->n_samples;
   const int tiles_y = (int)ceil_div(H, 16);
+  PhaseTimer pt(s, "reslice");
   Scratch<double> gate((size_t)P * a.n_orient, s);
   a.gate = gate.ptr;
   if (vol->n_orient > 0) {
@@ -201,7 +310,38 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
                                                                  d_params, P, *cfg, gate.ptr);
     DARE_CUDA(cudaGetLastError());
   }
-  reslice_k<<<dim3(a.tiles_x * tiles_y, P), 256, 0, s>>>(a, d_pixels, d_cov);
+  pt.mark("gate");
+  a.order = nullptr;
+  Scratch<int> order(P >= 4 ? P : 0, s);
+  if (P >= 4 && !brute) {
+    Scratch<unsigned long long> keys(2 * (size_t)P, s);
+    Scratch<int> idx(P, s);
+    pose_key_k<<<ceil_div(P, 128), 128, 0, s>>>(d_params, P, W, H, a.origin[0], a.origin[1],
+                                                 a.origin[2], 8.0 * a.voxel, keys.ptr, idx.ptr);
+    size_t bytes = 0;
+    DARE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.ptr, keys.ptr + P, idx.ptr,
+                                              order.ptr, P, 0, 60, s));
+    Scratch<uint8_t> tmp(bytes, s);
+    DARE_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, bytes, keys.ptr, keys.ptr + P, idx.ptr,
+                                              order.ptr, P, 0, 60, s));
+    a.order = order.ptr;
+  }
+  pt.mark("order");
+  const dim3 grid(a.tiles_x * tiles_y, P);
+  static bool attr_done = false;  // benign race: idempotent attribute set
+  if (!attr_done) {
+    DARE_CUDA(cudaFuncSetAttribute(reslice_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    DARE_CUDA(cudaFuncSetAttribute(reslice_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    DARE_CUDA(cudaFuncSetAttribute(reslice_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    attr_done = true;
+  }
+  if (a.dist_mode == 0)
+    reslice_k<0><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else if (a.dist_mode == 1)
+    reslice_k<1><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else
+    reslice_k<2><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  pt.mark("reslice_k");
   DARE_CUDA(cudaGetLastError());
 }
 

@@ -26,7 +26,31 @@ cudaStream_t thread_stream() {
   cudaStream_t s;
   DARE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   streams.by_dev[dev] = s;
+  static std::mutex mu;
+  static std::map<int, bool> pool_done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool_done[dev]) {
+    cudaMemPool_t pool;
+    DARE_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    DARE_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pool_done[dev] = true;
+  }
   return s;
+}
+
+void dev_alloc_bytes(void** p, size_t bytes) {
+  cudaStream_t s = thread_stream();
+  DARE_CUDA(cudaMallocAsync(p, bytes ? bytes : 1, s));
+  DARE_CUDA(cudaStreamSynchronize(s));  // usable from any stream once this returns
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  try {
+    cudaFreeAsync(p, thread_stream());
+  } catch (...) {
+  }
 }
 
 int sm_count() {
@@ -41,6 +65,36 @@ int sm_count() {
   DARE_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   cache[dev] = n;
   return n;
+}
+
+PhaseTimer::PhaseTimer(cudaStream_t s, const char* what) : s_(s), what_(what) {
+  const char* env = getenv("DARE_PROFILE");
+  on_ = env && env[0] && env[0] != '0';
+  if (on_) mark("start");
+}
+
+void PhaseTimer::mark(const char* phase) {
+  if (!on_ || n_ >= 32) return;
+  cudaEventCreate(&marks_[n_].ev);
+  cudaEventRecord(marks_[n_].ev, s_);
+  marks_[n_].name = phase;
+  ++n_;
+}
+
+PhaseTimer::~PhaseTimer() {
+  if (!on_) return;
+  mark("end");
+  cudaEventSynchronize(marks_[n_ - 1].ev);
+  float total = 0;
+  cudaEventElapsedTime(&total, marks_[0].ev, marks_[n_ - 1].ev);
+  fprintf(stderr, "[dare-profile] %s total %.3f ms:", what_, total);
+  for (int i = 1; i < n_; ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, marks_[i - 1].ev, marks_[i].ev);
+    fprintf(stderr, " %s=%.3f", marks_[i].name, ms);
+  }
+  fprintf(stderr, "\n");
+  for (int i = 0; i < n_; ++i) cudaEventDestroy(marks_[i].ev);
 }
 
 VoxelMap make_voxel_map(const double* origin, double voxel, const int64_t* dims) {
@@ -99,22 +153,24 @@ FrameSet::~FrameSet() {
 }  // namespace dare
 
 dare_volume_s::~dare_volume_s() {
+  using dare::dev_free;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  if (d_offsets) cudaFree(d_offsets);
-  if (d_records) cudaFree(d_records);
-  if (d_orient) cudaFree(d_orient);
+  dev_free(d_offsets);
+  dev_free(d_records);
+  dev_free(d_orient);
   cudaSetDevice(prev);
 }
 
 dare_scalar_s::~dare_scalar_s() {
+  using dare::dev_free;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  if (d_values) cudaFree(d_values);
-  if (d_flags) cudaFree(d_flags);
-  if (d_counts) cudaFree(d_counts);
+  dev_free(d_values);
+  dev_free(d_flags);
+  dev_free(d_counts);
   cudaSetDevice(prev);
 }
 

@@ -220,9 +220,9 @@ static std::unique_ptr<dare_scalar_s> new_scalar(const double* origin, double vo
   }
   sv->voxel = voxel;
   sv->ncells = dims[0] * dims[1] * dims[2];
-  DARE_CUDA(cudaMalloc(&sv->d_values, sizeof(float) * sv->ncells));
-  DARE_CUDA(cudaMalloc(&sv->d_flags, sv->ncells));
-  if (with_counts) DARE_CUDA(cudaMalloc(&sv->d_counts, sizeof(int64_t) * sv->ncells));
+  dev_alloc(&sv->d_values, sizeof(float) * sv->ncells);
+  dev_alloc(&sv->d_flags, sv->ncells);
+  if (with_counts) dev_alloc(&sv->d_counts, sizeof(int64_t) * sv->ncells);
   return sv;
 }
 

@@ -116,9 +116,9 @@ extern "C" int dare_volume_upload(const double* origin, double voxel_size, const
     vol->n_samples = n;
     vol->n_orient = (int64_t)table.size();
     cudaStream_t s = thread_stream();
-    DARE_CUDA(cudaMalloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1)));
-    DARE_CUDA(cudaMalloc(&vol->d_records, sizeof(uint4) * records.size()));
-    DARE_CUDA(cudaMalloc(&vol->d_orient, sizeof(float4) * std::max<size_t>(table.size(), 1)));
+    dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
+    dev_alloc(&vol->d_records, sizeof(uint4) * records.size());
+    dev_alloc(&vol->d_orient, sizeof(float4) * std::max<size_t>(table.size(), 1));
     DARE_CUDA(cudaMemcpyAsync(vol->d_offsets, offsets.data(), sizeof(uint32_t) * (ncells + 1),
                               cudaMemcpyHostToDevice, s));
     DARE_CUDA(cudaMemcpyAsync(vol->d_records, records.data(), sizeof(uint4) * records.size(),

@@ -125,10 +125,16 @@ _foreign: "weakref.WeakKeyDictionary[object, ScalarVolume]" = weakref.WeakKeyDic
 def as_device_scalar(volume) -> ScalarVolume:
     if isinstance(volume, ScalarVolume):
         return volume
-    cached = _foreign.get(volume)
+    def convert():
+        return ScalarVolume(volume.origin, volume.voxel_size, volume.dims, volume.values, volume.flags,
+                            getattr(volume, "counts", None))
+
+    try:
+        cached = _foreign.get(volume)
+    except TypeError:  # not weak-referenceable: no caching
+        return convert()
     if cached is None:
-        cached = ScalarVolume(volume.origin, volume.voxel_size, volume.dims, volume.values, volume.flags,
-                              getattr(volume, "counts", None))
+        cached = convert()
         _foreign[volume] = cached
     return cached
 

@@ -271,13 +271,20 @@ def as_device_volume(volume) -> DirectionalVolume:
     immutable, volume.py:89-92)."""
     if isinstance(volume, DirectionalVolume):
         return volume
+
+    def convert():
+        v = DirectionalVolume(volume.origin, volume.voxel_size, volume.dims, volume.cell_starts,
+                              volume.cell_counts, volume.positions, volume.orientations, volume.intensities)
+        v.rejected_out_of_bounds = getattr(volume, "rejected_out_of_bounds", 0)
+        return v
+
     with _foreign_lock:
-        cached = _foreign_cache.get(volume)
+        try:
+            cached = _foreign_cache.get(volume)
+        except TypeError:  # not weak-referenceable: no caching
+            return convert()
         if cached is None:
-            cached = DirectionalVolume(volume.origin, volume.voxel_size, volume.dims, volume.cell_starts,
-                                       volume.cell_counts, volume.positions, volume.orientations,
-                                       volume.intensities)
-            cached.rejected_out_of_bounds = getattr(volume, "rejected_out_of_bounds", 0)
+            cached = convert()
             _foreign_cache[volume] = cached
     return cached
 
