@@ -130,6 +130,20 @@ int dare_volume_seal(const double* origin, double voxel_size, const int64_t* dim
                      int64_t n_samples, const float* positions, const float* orientations,
                      const uint8_t* intensities, dare_volume_t* out);
 
+/* Frame-sharded reconstruction (multi-GPU): merges n_parts partial
+ * volumes built by dare_reconstruct over consecutive frame blocks into the
+ * SAME grid.  Parts are given as device buffers on the current device (the
+ * d_* views of dare_volume_info, or the same arrays received through NCCL):
+ * per part the ncells+1 offsets, the 16 B records, the orientation table and
+ * its sizes.  Within each cell the parts' runs are concatenated in part
+ * order, which is the reference's insertion order when part r holds frames
+ * after part r-1 -- the result is bit-identical to a single-device build. */
+int dare_volume_merge(const double* origin, double voxel_size, const int64_t* dims,
+                      int32_t n_parts, const uint32_t* const* d_offsets,
+                      const void* const* d_records, const float* const* d_orient,
+                      const int64_t* n_samples, const int64_t* n_orient, const int64_t* rejected,
+                      dare_volume_t* out);
+
 /* Uploads a sealed volume in the reference layout (volume.py:76-93, as
  * produced by VolumeBuilder.seal or load_volume volume.py:300-330):
  * cell_starts/cell_counts i64[ncells], positions f32[n,3], orientations
@@ -171,6 +185,18 @@ int dare_compound(const uint8_t* frames, int64_t n_images, int32_t height, int32
                   const double* frame_axes, double pitch_x, double pitch_y, const uint8_t* mask,
                   const double* origin, double voxel_size, const int64_t* dims,
                   dare_scalar_t* out);
+/* The two halves of dare_compound, for frame-sharded compounding: accumulate
+ * the frames' u64 intensity sums and observation counts into caller-owned,
+ * zero-initialised device arrays (ncells each; exact integers, so per-rank
+ * partials combine with an all-reduce SUM), then finalise values/flags. */
+int dare_compound_accumulate(const uint8_t* frames, int64_t n_images, int32_t height,
+                             int32_t width, int32_t frames_on_device, const int32_t* frame_image,
+                             int64_t n_frames, const double* frame_axes, double pitch_x,
+                             double pitch_y, const uint8_t* mask, const double* origin,
+                             double voxel_size, const int64_t* dims, uint64_t* d_sums,
+                             uint64_t* d_counts, void* stream);
+int dare_scalar_from_sums(const double* origin, double voxel_size, const int64_t* dims,
+                          const uint64_t* d_sums, const uint64_t* d_counts, dare_scalar_t* out);
 /* Uploads values f32 / flags u8 / counts i64 (counts may be NULL). */
 int dare_scalar_upload(const double* origin, double voxel_size, const int64_t* dims,
                        const float* values, const uint8_t* flags, const int64_t* counts,

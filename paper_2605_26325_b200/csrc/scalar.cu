@@ -253,6 +253,55 @@ static void launch_trilinear(dare_scalar_t vol, int32_t P, const double* d_param
 
 using namespace dare;
 
+// Accumulates integer intensity sums / observation counts of the given frames
+// into caller-owned device arrays (ncells u64 each).  Frame-sharded multi-GPU
+// compounding all-reduces these (exact integers) before finalising.
+extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images, int32_t height,
+                                        int32_t width, int32_t frames_on_device,
+                                        const int32_t* frame_image, int64_t n_frames,
+                                        const double* frame_axes, double pitch_x, double pitch_y,
+                                        const uint8_t* mask, const double* origin,
+                                        double voxel_size, const int64_t* dims, uint64_t* d_sums,
+                                        uint64_t* d_counts, void* stream) {
+  return guard([&] {
+    DARE_REQUIRE(d_sums != nullptr && d_counts != nullptr, "null accumulator");
+    DARE_REQUIRE(voxel_size > 0, "voxel_size must be > 0");
+    cudaStream_t s = stream ? (cudaStream_t)stream : thread_stream();
+    FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
+                frame_axes, pitch_x, pitch_y, mask, s);
+    VoxelMap m = make_voxel_map(origin, voxel_size, dims);
+    ScalarFrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
+                       fs.H,        fs.W,       fs.px,     fs.py};
+    const int64_t hw = (int64_t)height * width;
+    if (n_frames > 0) {
+      dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(n_frames, 65535));
+      compound_k<<<grid, 256, 0, s>>>(fv, m, (unsigned long long*)d_sums,
+                                      (unsigned long long*)d_counts);
+      DARE_CUDA(cudaGetLastError());
+    }
+    if (!frames_on_device || !stream) DARE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// values = f32(f64(sum) / f64(count)), flags 0/1, counts kept (baseline.py:93-96).
+extern "C" int dare_scalar_from_sums(const double* origin, double voxel_size, const int64_t* dims,
+                                     const uint64_t* d_sums, const uint64_t* d_counts,
+                                     dare_scalar_t* out) {
+  return guard([&] {
+    DARE_REQUIRE(out != nullptr, "out handle pointer is null");
+    cudaStream_t s = thread_stream();
+    auto sv = new_scalar(origin, voxel_size, dims, true);
+    DARE_CUDA(cudaMemcpyAsync(sv->d_counts, d_counts, sizeof(int64_t) * sv->ncells,
+                              cudaMemcpyDeviceToDevice, s));
+    compound_finalize_k<<<ceil_div(sv->ncells, 256), 256, 0, s>>>(
+        sv->ncells, (const unsigned long long*)d_sums, (const unsigned long long*)d_counts,
+        sv->d_values, sv->d_flags);
+    DARE_CUDA(cudaGetLastError());
+    DARE_CUDA(cudaStreamSynchronize(s));
+    *out = sv.release();
+  });
+}
+
 extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t height,
                              int32_t width, int32_t frames_on_device, const int32_t* frame_image,
                              int64_t n_frames, const double* frame_axes, double pitch_x,
@@ -260,27 +309,19 @@ extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t he
                              double voxel_size, const int64_t* dims, dare_scalar_t* out) {
   return guard([&] {
     DARE_REQUIRE(out != nullptr, "out handle pointer is null");
+    DARE_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
     cudaStream_t s = thread_stream();
-    FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
-                frame_axes, pitch_x, pitch_y, mask, s);
-    auto sv = new_scalar(origin, voxel_size, dims, true);
-    VoxelMap m = make_voxel_map(origin, voxel_size, dims);
-    Scratch<unsigned long long> sums(sv->ncells, s);
-    DARE_CUDA(cudaMemsetAsync(sums.ptr, 0, sizeof(unsigned long long) * sv->ncells, s));
-    DARE_CUDA(cudaMemsetAsync(sv->d_counts, 0, sizeof(int64_t) * sv->ncells, s));
-    ScalarFrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
-                       fs.H,        fs.W,       fs.px,     fs.py};
-    const int64_t hw = (int64_t)height * width;
-    if (n_frames > 0) {
-      dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(n_frames, 65535));
-      compound_k<<<grid, 256, 0, s>>>(fv, m, sums.ptr, (unsigned long long*)sv->d_counts);
-      DARE_CUDA(cudaGetLastError());
-    }
-    compound_finalize_k<<<ceil_div(sv->ncells, 256), 256, 0, s>>>(
-        sv->ncells, sums.ptr, (const unsigned long long*)sv->d_counts, sv->d_values, sv->d_flags);
-    DARE_CUDA(cudaGetLastError());
-    DARE_CUDA(cudaStreamSynchronize(s));
-    *out = sv.release();
+    const int64_t ncells = dims[0] * dims[1] * dims[2];
+    Scratch<unsigned long long> acc(2 * ncells, s);
+    DARE_CUDA(cudaMemsetAsync(acc.ptr, 0, sizeof(unsigned long long) * 2 * ncells, s));
+    int rc = dare_compound_accumulate(frames, n_images, height, width, frames_on_device,
+                                      frame_image, n_frames, frame_axes, pitch_x, pitch_y, mask,
+                                      origin, voxel_size, dims, (uint64_t*)acc.ptr,
+                                      (uint64_t*)(acc.ptr + ncells), (void*)s);
+    if (rc != DARE_OK) throw Error{rc, dare_last_error()};
+    rc = dare_scalar_from_sums(origin, voxel_size, dims, (const uint64_t*)acc.ptr,
+                               (const uint64_t*)(acc.ptr + ncells), out);
+    if (rc != DARE_OK) throw Error{rc, dare_last_error()};
   });
 }
 

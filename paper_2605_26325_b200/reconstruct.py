@@ -15,8 +15,52 @@ import numpy as np
 
 from . import _lib
 from .errors import InvalidArgumentError
-from .sweep import SweepRecording, grid_for, plan_frames, validate_margin
+from .sweep import FramePlan, SweepRecording, grid_for, plan_frames, validate_margin
 from .volume import DirectionalVolume, _Handle
+
+
+def frames_arg(sweep, frames_device_ptr: int | None = None):
+    """(images, pointer, on_device) for the image stack: a CUDA tensor or an
+    explicit device pointer is used in place, anything else is a host array."""
+    images = sweep.images
+    if frames_device_ptr is None and getattr(images, "is_cuda", False):
+        if images.dtype.itemsize != 1 or not images.is_contiguous():
+            raise InvalidArgumentError("device images must be a contiguous uint8 tensor")
+        frames_device_ptr = images.data_ptr()
+    if frames_device_ptr is not None:
+        return images, ctypes.c_void_p(int(frames_device_ptr)), 1
+    images = np.ascontiguousarray(np.asarray(images), dtype=np.uint8)
+    return images, _lib.vptr(images), 0
+
+
+def _mask(sweep):
+    if sweep.mask is None:
+        return None
+    return np.ascontiguousarray(np.asarray(sweep.mask, dtype=bool).reshape(-1).astype(np.uint8))
+
+
+def reconstruct_subset(sweep, plan: FramePlan, start: int, end: int, origin, voxel: float, dims,
+                       frames_device_ptr: int | None = None) -> DirectionalVolume:
+    """Synchronized frames [start, end) into the given grid (the full grid for
+    frame-sharded multi-GPU builds; start=0, end=n for a whole sweep)."""
+    images, frames_ptr, on_device = frames_arg(sweep, frames_device_ptr)
+    idx = np.ascontiguousarray(plan.image_index[start:end])
+    axes = np.ascontiguousarray(plan.axes()[start:end])
+    quats = np.ascontiguousarray(plan.canonical_quats_f32()[start:end])
+    mask = _mask(sweep)
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    raw = ctypes.c_void_p()
+    rejected = ctypes.c_int64(0)
+    _lib.call("dare_reconstruct", frames_ptr, int(images.shape[0]), int(plan.height), int(plan.width),
+              on_device, _lib.ptr(idx, ctypes.c_int32), int(end - start),
+              _lib.ptr(axes, ctypes.c_double), _lib.ptr(quats, ctypes.c_float),
+              plan.pixel_pitch[0], plan.pixel_pitch[1], _lib.ptr(mask, ctypes.c_uint8),
+              _lib.ptr(o, ctypes.c_double), float(voxel), _lib.ptr(d, ctypes.c_int64), ctypes.byref(raw),
+              ctypes.byref(rejected))
+    vol = DirectionalVolume(origin, voxel, dims, _handle=_Handle(raw.value))
+    vol.rejected_out_of_bounds = int(rejected.value)
+    return vol
 
 
 def reconstruct_volume(sweep: SweepRecording, voxel_size: float = 0.125, margin: float = 1.0,
@@ -30,34 +74,4 @@ def reconstruct_volume(sweep: SweepRecording, voxel_size: float = 0.125, margin:
     validate_margin(margin)
     plan = plan_frames(sweep)
     origin, voxel, dims = grid_for(plan, voxel_size, margin)
-    images = sweep.images
-    if frames_device_ptr is None and getattr(images, "is_cuda", False):
-        if images.dtype.itemsize != 1 or not images.is_contiguous():
-            raise InvalidArgumentError("device images must be a contiguous uint8 tensor")
-        frames_device_ptr = images.data_ptr()
-    if frames_device_ptr is None:
-        images = np.asarray(images)
-        images = np.ascontiguousarray(images, dtype=np.uint8)
-        frames_arg = _lib.vptr(images)
-        on_device = 0
-    else:
-        frames_arg = ctypes.c_void_p(int(frames_device_ptr))
-        on_device = 1
-    mask = None
-    if sweep.mask is not None:
-        mask = np.ascontiguousarray(np.asarray(sweep.mask, dtype=bool).reshape(-1).astype(np.uint8))
-    axes = plan.axes()
-    quats = plan.canonical_quats_f32()
-    o = np.ascontiguousarray(origin, dtype=np.float64)
-    d = np.ascontiguousarray(dims, dtype=np.int64)
-    raw = ctypes.c_void_p()
-    rejected = ctypes.c_int64(0)
-    _lib.call("dare_reconstruct", frames_arg, int(images.shape[0]), int(plan.height), int(plan.width),
-              on_device, _lib.ptr(plan.image_index, ctypes.c_int32), plan.n_frames,
-              _lib.ptr(axes, ctypes.c_double), _lib.ptr(quats, ctypes.c_float),
-              plan.pixel_pitch[0], plan.pixel_pitch[1], _lib.ptr(mask, ctypes.c_uint8),
-              _lib.ptr(o, ctypes.c_double), voxel, _lib.ptr(d, ctypes.c_int64), ctypes.byref(raw),
-              ctypes.byref(rejected))
-    vol = DirectionalVolume(origin, voxel, dims, _handle=_Handle(raw.value))
-    vol.rejected_out_of_bounds = int(rejected.value)
-    return vol
+    return reconstruct_subset(sweep, plan, 0, plan.n_frames, origin, voxel, dims, frames_device_ptr)

@@ -144,7 +144,9 @@ def compound(sweep, voxel_size: float = 0.125, margin: float = 1.0) -> ScalarVol
     validate_margin(margin)
     plan = plan_frames(sweep)
     origin, voxel, dims = grid_for(plan, voxel_size, margin)
-    images = np.ascontiguousarray(np.asarray(sweep.images), dtype=np.uint8)
+    from .reconstruct import frames_arg
+
+    images, frames_ptr, on_device = frames_arg(sweep)
     mask = None
     if sweep.mask is not None:
         mask = np.ascontiguousarray(np.asarray(sweep.mask, dtype=bool).reshape(-1).astype(np.uint8))
@@ -152,7 +154,7 @@ def compound(sweep, voxel_size: float = 0.125, margin: float = 1.0) -> ScalarVol
     o = np.ascontiguousarray(origin, dtype=np.float64)
     d = np.ascontiguousarray(dims, dtype=np.int64)
     raw = ctypes.c_void_p()
-    _lib.call("dare_compound", _lib.vptr(images), int(images.shape[0]), plan.height, plan.width, 0,
+    _lib.call("dare_compound", frames_ptr, int(images.shape[0]), plan.height, plan.width, on_device,
               _lib.ptr(plan.image_index, ctypes.c_int32), plan.n_frames, _lib.ptr(axes, ctypes.c_double),
               plan.pixel_pitch[0], plan.pixel_pitch[1], _lib.ptr(mask, ctypes.c_uint8),
               _lib.ptr(o, ctypes.c_double), voxel, _lib.ptr(d, ctypes.c_int64), ctypes.byref(raw))
