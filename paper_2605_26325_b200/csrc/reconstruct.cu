@@ -5,16 +5,22 @@
 // volume.py:240-269 (seal: stable argsort by linear cell + bincount + cumsum).
 //
 // Device pipeline (all FP64 chains bit-identical to numpy; -fmad=false):
-//   1. count   : per pixel -> cell; warp-aggregated u32 histogram
-//                (__match_any_sync groups equal cells, one atomic per group);
-//                out-of-bounds pixels counted (volume.py:230-233).
-//   2. scan    : exclusive prefix of counts -> cell offsets (CUB).
-//   3. fill    : per pixel -> slot = offset + atomic cursor; stores the pixel's
-//                global insertion key (synchronized frame * H*W + pixel).
-//   4. seal    : per cell, sort its (tiny) key run ascending = insertion order
-//                (this is what makes the atomic fill identical to numpy's
-//                stable argsort) and materialise the 16 B records; runs > 32
-//                keys go through CUB's segmented sort.
+//   1. count : per pixel -> cell; warp-aggregated u32 histogram
+//              (__match_any_sync groups equal cells, one atomic per group);
+//              out-of-bounds pixels counted (volume.py:230-233).
+//   2. scan  : exclusive prefix of counts -> cell offsets (CUB).
+//   3. fill  : per pixel -> slot = offset + atomic cursor; stores the 64-bit
+//              key (insertion index << 8 | intensity); the insertion index is
+//              synchronized frame * H*W + row-major pixel.
+//   4. seal  : per cell, sort its (tiny) key run ascending = insertion order --
+//              this is what makes the atomic fill identical to numpy's stable
+//              argsort -- and materialise the 16 B records.  A warp seals 32
+//              consecutive cells: their keys are staged in shared memory with
+//              coalesced loads, each lane sorts its cell, and the records are
+//              written back coalesced.  Runs longer than 32 go through CUB's
+//              segmented sort and are (re)written afterwards.
+// All pixel/cell index math is 32-bit (dims < 2^31 cells, < 2^32 pixels) with
+// a multiply-high divider, which keeps the per-pixel instruction count low.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
@@ -25,76 +31,119 @@
 
 namespace dare {
 
+// n / d for every 32-bit n (round-up multiply-high with the "add" fix-up).
+struct FastDiv {
+  uint32_t d = 1, mul = 0, shift = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    if (d <= 1) return;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    mul = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    shift = l;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    if (d == 1) return n;
+    const uint32_t t = __umulhi(n, mul);
+    return (t + ((n - t) >> 1)) >> (shift - 1);
+  }
+};
+
 struct FrameView {
   const uint8_t* frames;
   const int32_t* image;
   const double* axes;
   const uint8_t* mask;
-  int64_t n_frames;
-  int32_t H, W;
+  uint32_t n_frames;
+  uint32_t H, W, hw;
   double px, py;
   const uint32_t* oid;  // orientation id per synchronized frame
+  FastDiv div_w, div_hw;
 };
 
-static FrameView view_of(const FrameSet& fs) {
-  return FrameView{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
-                   fs.H,        fs.W,       fs.px,     fs.py,      nullptr};
+// Pixel (u, v) of a frame with axes fa = {c0[3], c1[3], t[3]}: f32 world
+// position (reconstruct.py:156-162) and linear cell, or -1 when out of bounds.
+__device__ __forceinline__ int32_t pixel_cell32(const double* __restrict__ fa, uint32_t u,
+                                                uint32_t v, double px, double py,
+                                                const VoxelMap& m) {
+  const double U = (double)u * px, V = (double)v * py;
+  bool ok = true;
+  uint32_t idx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float p32 = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
+    const double f = floor(voxel_coord(m, a, p32));
+    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
+    idx[a] = ok ? (uint32_t)f : 0u;
+  }
+  return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // Warp-aggregated histogram (kFill=false) or slot assignment (kFill=true):
 // lanes holding the same cell form one __match_any_sync group; the lowest lane
-// does one atomic for the whole group and lanes take consecutive slots in lane
-// order (= insertion order within the warp).
+// does one atomic for the whole group and lanes take consecutive slots.
 template <bool kFill>
-__device__ __forceinline__ void warp_scatter(bool kept, int64_t lin, uint32_t key,
+__device__ __forceinline__ void warp_scatter(bool kept, int32_t lin, unsigned long long key,
                                              uint32_t* counts,
                                              const uint32_t* __restrict__ offsets,
-                                             uint32_t* keys) {
-  unsigned active = __ballot_sync(0xffffffffu, kept);
+                                             unsigned long long* keys) {
+  const unsigned active = __ballot_sync(0xffffffffu, kept);
   if (!kept) return;
-  unsigned peers = __match_any_sync(active, (unsigned long long)lin);
-  unsigned leader = __ffs(peers) - 1;
-  unsigned n = __popc(peers);
+  const unsigned peers = __match_any_sync(active, (unsigned)lin);
+  const unsigned leader = __ffs(peers) - 1;
+  const unsigned n = __popc(peers);
   if (!kFill) {
     if (lane_id() == leader) atomicAdd(&counts[lin], n);
   } else {
     unsigned base = 0;
     if (lane_id() == leader) base = atomicAdd(&counts[lin], n);
     base = __shfl_sync(peers, base, leader);
-    unsigned rank = __popc(peers & ((1u << lane_id()) - 1u));
+    const unsigned rank = __popc(peers & ((1u << lane_id()) - 1u));
     keys[offsets[lin] + base + rank] = key;
   }
 }
 
-// Frames: grid x over pixel blocks of one frame, y over frames (strided).
+// Frames: a block covers a 16(u) x 4(v) x 4(frames) brick of pixels and each
+// warp an 8 x 2 x 2 sub-brick, so that pixels landing in the same cell --
+// neighbours in the image and in consecutive frames of a sweep -- meet in one
+// warp and share one atomic.  (Slot order inside a cell is irrelevant: seal
+// sorts every run by insertion key.)  grid: x = (u,v) tiles, y = frame groups.
+constexpr int kBrickU = 16, kBrickV = 4, kBrickF = 4;
+
 template <bool kFill>
 __global__ void __launch_bounds__(256) frame_scatter_k(FrameView fv, VoxelMap m,
                                                        uint32_t* counts,
                                                        const uint32_t* __restrict__ offsets,
-                                                       uint32_t* keys,
+                                                       unsigned long long* keys,
                                                        unsigned long long* rejected) {
-  __shared__ double s_axes[9];
-  const int64_t hw = (int64_t)fv.H * fv.W;
-  for (int64_t f = blockIdx.y; f < fv.n_frames; f += gridDim.y) {
-    __syncthreads();
-    if (threadIdx.x < 9) s_axes[threadIdx.x] = fv.axes[f * 9 + threadIdx.x];
-    __syncthreads();
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool valid = p < hw;
-    if (valid && fv.mask) valid = fv.mask[p] != 0;
-    int64_t lin = -1;
-    if (valid) {
-      float p32[3];
-      lin = pixel_cell(s_axes, (int)(p % fv.W), (int)(p / fv.W), fv.px, fv.py, m, p32);
-    }
-    bool kept = lin >= 0;
+  // No block barriers: each warp strides over its frames independently, so the
+  // latency of one frame's (returning) atomics overlaps other warps' work.
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t tiles_u = (fv.W + kBrickU - 1) / kBrickU;
+  const uint32_t tu = blockIdx.x % tiles_u, tv = blockIdx.x / tiles_u;
+  const uint32_t u = tu * kBrickU + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = tv * kBrickV + ((warp >> 1) & 1) * 2 + ((lane >> 3) & 1);
+  const uint32_t fl = (warp >> 2) * 2 + (lane >> 4);  // frame within the brick
+  const uint32_t p = v * fv.W + u;
+  const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
+  const double* __restrict__ axes = fv.axes;
+  for (uint32_t f0 = blockIdx.y * kBrickF; f0 < fv.n_frames; f0 += gridDim.y * kBrickF) {
+    const uint32_t f = f0 + fl;
+    const bool valid = in_frame && f < fv.n_frames;
+    const int32_t lin = valid ? pixel_cell32(axes + (size_t)f * 9, u, v, fv.px, fv.py, m) : -1;
+    const bool kept = lin >= 0;
     if (!kFill) {
-      int oob = __syncthreads_count(valid && !kept);
-      if (threadIdx.x == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
+      const unsigned oob = __ballot_sync(0xffffffffu, valid && !kept);
+      if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
     }
-    warp_scatter<kFill>(kept, lin, (uint32_t)(f * hw + p), counts, offsets, keys);
+    unsigned long long key = 0;
+    if (kFill && kept) {
+      const uint32_t inten = fv.frames[(size_t)fv.image[f] * fv.hw + p];
+      key = ((unsigned long long)(f * fv.hw + p) << 8) | inten;
+    }
+    warp_scatter<kFill>(kept, lin, key, counts, offsets, keys);
   }
 }
 
@@ -103,84 +152,132 @@ template <bool kFill>
 __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict__ pos, int64_t n,
                                                         VoxelMap m, uint32_t* counts,
                                                         const uint32_t* __restrict__ offsets,
-                                                        uint32_t* keys,
+                                                        unsigned long long* keys,
                                                         unsigned long long* rejected) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = i < n;
-  int64_t lin = -1;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  int32_t lin = -1;
   if (valid) {
     bool ok = true;
-    int64_t idx[3];
+    uint32_t idx[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double f = floor(voxel_coord(m, a, pos[3 * i + a]));
+      const double f = floor(voxel_coord(m, a, pos[3 * i + a]));
       ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
-      idx[a] = ok ? (int64_t)f : 0;
+      idx[a] = ok ? (uint32_t)f : 0u;
     }
-    if (ok) lin = (idx[0] * m.dims[1] + idx[1]) * m.dims[2] + idx[2];
+    if (ok) lin = (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]);
   }
-  bool kept = lin >= 0;
+  const bool kept = lin >= 0;
   if (!kFill) {
-    int oob = __syncthreads_count(valid && !kept);
+    const int oob = __syncthreads_count(valid && !kept);
     if (threadIdx.x == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
   }
-  warp_scatter<kFill>(kept, lin, (uint32_t)i, counts, offsets, keys);
+  warp_scatter<kFill>(kept, lin, (unsigned long long)i, counts, offsets, keys);
 }
 
 struct FrameRecords {
   FrameView fv;
-  __device__ __forceinline__ uint4 operator()(uint32_t key) const {
-    const uint32_t hw = (uint32_t)fv.H * (uint32_t)fv.W;
-    uint32_t f = key / hw, p = key - f * hw;
-    int u = (int)(p % (uint32_t)fv.W), v = (int)(p / (uint32_t)fv.W);
+  __device__ __forceinline__ uint4 operator()(unsigned long long key) const {
+    const uint32_t pid = (uint32_t)(key >> 8);
+    const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
+    const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
     const double* fa = fv.axes + (size_t)f * 9;
-    double U = (double)u * fv.px, V = (double)v * fv.py;
+    const double U = (double)u * fv.px, V = (double)v * fv.py;
     float p32[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
       p32[a] = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
-    uint8_t inten = fv.frames[(size_t)fv.image[f] * hw + p];
     return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
-                      (fv.oid[f] << 8) | inten);
+                      (fv.oid[f] << 8) | (uint32_t)(key & 0xffu));
   }
 };
 
 struct SampleRecords {
   const float* pos;
   const uint32_t* word;  // (oid << 8) | intensity
-  __device__ __forceinline__ uint4 operator()(uint32_t key) const {
-    return make_uint4(__float_as_uint(pos[3 * (size_t)key]), __float_as_uint(pos[3 * (size_t)key + 1]),
-                      __float_as_uint(pos[3 * (size_t)key + 2]), word[key]);
+  __device__ __forceinline__ uint4 operator()(unsigned long long key) const {
+    const size_t i = (size_t)key;
+    return make_uint4(__float_as_uint(pos[3 * i]), __float_as_uint(pos[3 * i + 1]),
+                      __float_as_uint(pos[3 * i + 2]), word[i]);
   }
 };
 
-constexpr int kSmallRun = 32;
+constexpr int kSmallRun = 32;  // per-cell runs sorted in shared memory by one lane
+constexpr int kSealWarps = 4;  // warps per seal block
+constexpr int kPitch = 33;     // odd row pitch (in u64): both access patterns conflict-free
 
-// thread per cell: sort the run's keys (= insertion order) and write records
+struct SealSmem {
+  unsigned long long st[kSmallRun * kPitch];  // st[k * kPitch + lane] = k-th key of cell c0+lane
+  uint16_t cstart[32];                         // cell start relative to the warp's first key
+  uint8_t cell_of[kSmallRun * 32];             // key position -> lane of its cell (0xff: big run)
+};
+
+// Warp seals cells [c0, c0+32).  Keys are loaded coalesced into a transposed,
+// padded stage (cell = column), each lane insertion-sorts its column (runs are
+// ~16 keys; the padded pitch makes the lanes' row accesses bank-conflict
+// free), and the records are written back coalesced in storage order.  Runs
+// longer than kSmallRun are listed for the CUB segmented-sort path.
 template <class Rec>
-__global__ void __launch_bounds__(256) seal_k(Rec rec, const uint32_t* __restrict__ offsets,
-                                              const uint32_t* __restrict__ keys, int64_t ncells,
-                                              uint4* records, uint32_t* big_cells,
-                                              uint32_t* n_big) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncells) return;
-  uint32_t s0 = offsets[c], n = offsets[c + 1] - s0;
-  if (n == 0) return;
-  if (n > kSmallRun) {
-    big_cells[atomicAdd(n_big, 1u)] = (uint32_t)c;
-    return;
+__global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
+                                                          const uint32_t* __restrict__ offsets,
+                                                          const unsigned long long* __restrict__ keys,
+                                                          uint32_t ncells, uint4* records,
+                                                          uint32_t* big_cells, uint32_t* n_big) {
+  __shared__ SealSmem smem[kSealWarps];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  SealSmem& sm = smem[warp];
+  const uint32_t c0 = (blockIdx.x * kSealWarps + warp) * 32u;
+  if (c0 >= ncells) return;
+  const uint32_t c = c0 + lane;
+  const uint32_t c_end = min(c0 + 32u, ncells);
+  const uint32_t s0 = offsets[c0], s1 = offsets[c_end];
+  uint32_t cs = 0, cn = 0;
+  if (c < ncells) {
+    cs = offsets[c];
+    cn = offsets[c + 1] - cs;
   }
-  uint32_t k[kSmallRun];
-  for (uint32_t i = 0; i < n; ++i) {
-    uint32_t x = keys[s0 + i];
-    uint32_t j = i;
-    while (j > 0 && k[j - 1] > x) {
-      k[j] = k[j - 1];
-      --j;
+  const bool big = cn > kSmallRun;
+  if (big) big_cells[atomicAdd(n_big, 1u)] = c;
+  const uint32_t len = s1 - s0;
+  const bool staged = !__any_sync(0xffffffffu, big);  // then len <= 32 * 32
+  if (staged) {
+    sm.cstart[lane] = (uint16_t)(cs - s0);
+    for (uint32_t k = 0; k < cn; ++k) sm.cell_of[cs - s0 + k] = (uint8_t)lane;
+    __syncwarp();
+    for (uint32_t i = lane; i < len; i += 32) {
+      const uint32_t col = sm.cell_of[i];
+      sm.st[(i - sm.cstart[col]) * kPitch + col] = keys[s0 + i];
     }
-    k[j] = x;
+    __syncwarp();
+    for (uint32_t i = 1; i < cn; ++i) {
+      const unsigned long long x = sm.st[i * kPitch + lane];
+      uint32_t j = i;
+      while (j > 0 && sm.st[(j - 1) * kPitch + lane] > x) {
+        sm.st[j * kPitch + lane] = sm.st[(j - 1) * kPitch + lane];
+        --j;
+      }
+      sm.st[j * kPitch + lane] = x;
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < len; i += 32) {
+      const uint32_t col = sm.cell_of[i];
+      records[s0 + i] = rec(sm.st[(i - sm.cstart[col]) * kPitch + col]);
+    }
+  } else if (cn > 0 && !big) {
+    // a big run in this warp's chunk: the small runs are sealed lane by lane
+    unsigned long long k[kSmallRun];
+    for (uint32_t i = 0; i < cn; ++i) {
+      const unsigned long long x = keys[cs + i];
+      uint32_t j = i;
+      while (j > 0 && k[j - 1] > x) {
+        k[j] = k[j - 1];
+        --j;
+      }
+      k[j] = x;
+    }
+    for (uint32_t i = 0; i < cn; ++i) records[cs + i] = rec(k[i]);
   }
-  for (uint32_t i = 0; i < n; ++i) records[s0 + i] = rec(k[i]);
 }
 
 __global__ void big_bounds_k(const uint32_t* big_cells, uint32_t n_big,
@@ -196,7 +293,7 @@ __global__ void big_bounds_k(const uint32_t* big_cells, uint32_t n_big,
 // block per big cell: records from the segment-sorted keys
 template <class Rec>
 __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_t* ends,
-                                  const uint32_t* __restrict__ sorted, uint4* records) {
+                                  const unsigned long long* __restrict__ sorted, uint4* records) {
   uint32_t b = begins[blockIdx.x], e = ends[blockIdx.x];
   for (uint32_t s = b + threadIdx.x; s < e; s += blockDim.x) records[s] = rec(sorted[s]);
 }
@@ -213,7 +310,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   DARE_CUDA(cudaMemsetAsync(rej.ptr, 0, sizeof(unsigned long long), s));
   dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
   pt.mark("alloc+memset");
-  scatter(false, counts.ptr, (const uint32_t*)nullptr, (uint32_t*)nullptr, rej.ptr);
+  scatter(false, counts.ptr, (const uint32_t*)nullptr, (unsigned long long*)nullptr, rej.ptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
   size_t tmp_bytes = 0;
@@ -235,7 +332,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   vol->rejected = (int64_t)n_rej;
   dev_alloc(&vol->d_records, sizeof(uint4) * std::max<uint32_t>(n_kept, 1));
   if (n_kept == 0) return;
-  Scratch<uint32_t> keys(n_kept, s);
+  Scratch<unsigned long long> keys(n_kept, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncells, s));
   pt.mark("readback+alloc");
   scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, keys.ptr,
@@ -245,8 +342,8 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   uint32_t* big_cells = counts.ptr;  // reuse: #big runs <= ncells
   Scratch<uint32_t> n_big_d(1, s);
   DARE_CUDA(cudaMemsetAsync(n_big_d.ptr, 0, sizeof(uint32_t), s));
-  seal_k<<<ceil_div(ncells, 256), 256, 0, s>>>(rec, vol->d_offsets, keys.ptr, ncells,
-                                                vol->d_records, big_cells, n_big_d.ptr);
+  seal_k<<<ceil_div(ncells, 32 * kSealWarps), 32 * kSealWarps, 0, s>>>(
+      rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("seal");
   uint32_t n_big = 0;
@@ -254,7 +351,8 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   DARE_CUDA(cudaStreamSynchronize(s));
   if (n_big == 0) return;
   DARE_LIMIT(n_kept < (uint32_t)INT32_MAX, "segmented sort limited to 2^31 samples");
-  Scratch<uint32_t> begins(n_big, s), ends(n_big, s), sorted(n_kept, s);
+  Scratch<uint32_t> begins(n_big, s), ends(n_big, s);
+  Scratch<unsigned long long> sorted(n_kept, s);
   big_bounds_k<<<ceil_div(n_big, 256), 256, 0, s>>>(big_cells, n_big, vol->d_offsets,
                                                     begins.ptr, ends.ptr);
   size_t sort_bytes = 0;
@@ -303,7 +401,6 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     cudaStream_t s = thread_stream();
     FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
                 frame_axes, pitch_x, pitch_y, mask, s);
-    FrameView fv = view_of(fs);
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
     // frames sharing a canonical f32 quaternion share an orientation id, so the
     // reslice gate table stays tiny for sweeps with few distinct orientations
@@ -315,16 +412,21 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     Scratch<uint32_t> d_oid((size_t)std::max<int64_t>(n_frames, 1), s);
     DARE_CUDA(cudaMemcpyAsync(d_oid.ptr, word.data(), sizeof(uint32_t) * word.size(),
                               cudaMemcpyHostToDevice, s));
-    fv.oid = d_oid.ptr;
+    FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
+                 (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
+                 FastDiv((uint32_t)width), FastDiv((uint32_t)hw)};
     vol->n_orient = (int64_t)table.size();
     if (!table.empty()) {
       dev_alloc(&vol->d_orient, sizeof(float4) * table.size());
       DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
                                 cudaMemcpyHostToDevice, s));
     }
-    dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(std::max<int64_t>(n_frames, 1), 65535));
-    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, uint32_t* keys,
-                       unsigned long long* rej) {
+    // a block keeps its (u, v) brick and strides over frame groups, so the
+    // per-thread setup is amortised over many frames
+    dim3 grid(ceil_div(width, kBrickU) * ceil_div(height, kBrickV),
+              (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n_frames, kBrickF), 1), 8));
+    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
+                       unsigned long long* keys, unsigned long long* rej) {
       if (n_frames == 0) return;
       if (fill)
         frame_scatter_k<true><<<grid, 256, 0, s>>>(fv, m, counts, offsets, keys, rej);
@@ -369,8 +471,8 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
     }
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
     const float* pos = d_pos.ptr;
-    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, uint32_t* keys,
-                       unsigned long long* rej) {
+    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
+                       unsigned long long* keys, unsigned long long* rej) {
       if (n_samples == 0) return;
       if (fill)
         sample_scatter_k<true><<<ceil_div(n_samples, 256), 256, 0, s>>>(pos, n_samples, m, counts,
