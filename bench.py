@@ -156,6 +156,25 @@ def cells_visited(torch, dims, origin, voxel, p14, W, H, radius):
     return torch.unique(torch.cat(cells))
 
 
+def _pow2(x: float) -> bool:
+    m, _ = math.frexp(x)
+    return x > 0 and m == 0.5
+
+
+def ncu_traffic(kernel: str, batch: int, config: str):
+    """DRAM bytes (read+write) per launch of `kernel` from the committed ncu capture
+    (profiles/round1_traffic.json, cfg2 with 64 poses per launch), or None."""
+    path = os.path.join(ROOT, "profiles", "round1_traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        if config != "cfg2" or batch != 64:
+            return None, "ncu capture is for cfg2 / 64 poses per launch"
+        return float(data["dram_bytes_per_launch"][kernel]), "profiles/round1_traffic.json (" + data["source"] + ")"
+    except Exception as e:  # noqa: BLE001
+        return None, f"no ncu capture ({type(e).__name__})"
+
+
 def make_rank_info():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -404,6 +423,7 @@ def run_b200(args):
         ref_bytes += 12 * len(cells) + 29 * float(c.sum().item()) + H * W * (1 + 1 / 8)
         own_bytes += 4 * len(cells) + 16 * float(c.sum().item()) + H * W * 2
     peak, peak_kind = hbm_peak()
+    traffic, traffic_src = ncu_traffic(f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>", B, args.config)
     achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
 
     # ---- CPU baseline (rank 0, bounded sample) ----
@@ -437,7 +457,8 @@ def run_b200(args):
             "e2e": {"value": e2e_value, "unit": "reslices/s", "h2d_bytes_per_step": B * 14 * 8,
                     "d2h_bytes_per_step": 2 * B * H * W},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "reslice_k (+gate_k)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "reslice_k (+gate_k)",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_step_ref_layout": ref_bytes,
                          "compulsory_bytes_per_step_own_layout": own_bytes},
