@@ -197,26 +197,37 @@ __global__ void __launch_bounds__(256) reslice_k(ResliceArgs a, uint8_t* __restr
     return false;
   };
   bool live = active && (a.brute ? true : (lox <= hix && loy <= hiy && loz <= hiz)) && open_run();
-  uint4 nxt = make_uint4(0, 0, 0, 0);
-  if (live) nxt = __ldg(a.records + s);
+  auto keep = [&](const uint4& c) -> bool {
+    const float x = __uint_as_float(c.x), y = __uint_as_float(c.y), z = __uint_as_float(c.z);
+    return x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi &&
+           (!gate_filter || gate[c.w >> 8] != CUDART_INF);
+  };
 
+  // Each lane holds a batch of up to 4 consecutive records of its current run
+  // (4 independent loads in flight) and a bit mask of the batch's survivors.
+  // Rounds: lanes with an exhausted batch refill (cheap, divergent); then
+  // every lane with a pending survivor evaluates it (converged FP64 path).
+  uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
+  unsigned mask = 0;
   double wsum = 0.0, iwsum = 0.0;
   while (true) {
-    bool found = false;
-    uint4 cur;
-    while (live) {
-      cur = nxt;
-      if (++s == e) live = open_run();
-      if (live) nxt = __ldg(a.records + s);  // prefetch the next visit
-      const float x = __uint_as_float(cur.x), y = __uint_as_float(cur.y), z = __uint_as_float(cur.z);
-      if (x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi &&
-          (!gate_filter || gate[cur.w >> 8] != CUDART_INF)) {
-        found = true;
-        break;
-      }
+    while (live && mask == 0) {
+      const uint32_t n = min(4u, e - s);
+      const uint4* __restrict__ q = a.records + s;
+      r0 = __ldg(q);
+      if (n > 1) r1 = __ldg(q + 1);
+      if (n > 2) r2 = __ldg(q + 2);
+      if (n > 3) r3 = __ldg(q + 3);
+      s += n;
+      mask = (keep(r0) ? 1u : 0u) | ((n > 1 && keep(r1)) ? 2u : 0u) | ((n > 2 && keep(r2)) ? 4u : 0u) |
+             ((n > 3 && keep(r3)) ? 8u : 0u);
+      if (s == e) live = open_run();
     }
-    if (!__any_sync(0xffffffffu, found)) break;
-    if (found) {
+    if (!__any_sync(0xffffffffu, mask != 0)) break;
+    if (mask) {
+      const unsigned kk = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint4 cur = kk == 0 ? r0 : (kk == 1 ? r1 : (kk == 2 ? r2 : r3));
       const double dx = (double)__uint_as_float(cur.x) - wx;
       const double dy = (double)__uint_as_float(cur.y) - wy;
       const double dz = (double)__uint_as_float(cur.z) - wz;
