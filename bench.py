@@ -406,7 +406,13 @@ def run_b200(args):
     params_d = torch.from_numpy(params).cuda()
     H = W = wl.plane
     out_d = torch.empty((2, B, H, W), dtype=torch.uint8, device="cuda")
-    kc = kernel_cfg(cfg)
+    # schedule for the device-pointer path: pose-major when the batch is a
+    # coherent trajectory (what dare_reslice decides by itself on host params)
+    p0 = params[args.warmup * B:(args.warmup + 1) * B]
+    coherent = _lib.load().dare_poses_coherent(p0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B, W, H,
+                                               float(wl.voxel))
+    schedule = 2 if coherent else 1
+    kc = kernel_cfg(cfg, schedule)
     # a real (non-default) stream: the kernels and the timing events share it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -504,6 +510,7 @@ def run_b200(args):
             "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> dims {dims} "
                                    f"({info.n_samples} samples), {B} poses/step at {W}x{H}, r={cfg.interp_radius}",
                        "poses_per_step": B, "parallelism": f"pose-sharded x{ws} (replicated volume)",
+                       "schedule": "pose-major" if schedule == 2 else "pixel-major",
                        "l2": "inputs larger than L2 (volume records "
                              f"{info.n_samples * 16 / 1e9:.1f} GB; each step's poses touch "
                              f"{own_bytes / 1e9:.2f} GB)"},

@@ -62,7 +62,9 @@ typedef struct {
   double k_inplane;
   double k_dist;
   int32_t unassigned;
-  int32_t _pad;
+  int32_t schedule; /* 0 auto, 1 pixel-major (spatially sorted batch), 2 pose-major
+                       (lanes = one pixel of 32 consecutive poses; for coherent
+                       trajectories).  Results are identical; only speed differs. */
 } dare_reslice_cfg;
 
 typedef struct {
@@ -175,6 +177,12 @@ int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const double* pa
 int dare_reslice_device(dare_volume_t vol, int32_t n_poses, const double* d_params,
                         int32_t width, int32_t height, const dare_reslice_cfg* cfg,
                         uint8_t* d_pixels, uint8_t* d_coverage, void* stream);
+
+/* 1 when consecutive planes of the batch are close (centre within one voxel,
+ * rotation within ~3 degrees) for >= 90% of pairs and n_poses >= 32: the
+ * pose-major schedule then shares every load across the warp.  Host params. */
+int dare_poses_coherent(const double* params, int32_t n_poses, int32_t width, int32_t height,
+                        double voxel_size);
 
 /* ---- scalar (direction-blind) arm -------------------------------------- */
 

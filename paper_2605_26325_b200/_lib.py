@@ -40,7 +40,7 @@ class ResliceCfg(ctypes.Structure):
     _fields_ = [
         ("radius", c_f64), ("cos_normal", c_f64), ("cos_inplane", c_f64),
         ("k_normal", c_f64), ("k_inplane", c_f64), ("k_dist", c_f64),
-        ("unassigned", c_i32), ("_pad", c_i32),
+        ("unassigned", c_i32), ("schedule", c_i32),
     ]
 
 
@@ -85,6 +85,7 @@ _SIGNATURES = {
     "dare_reslice": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_bruteforce": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8,
                                 P_u8],
+    "dare_poses_coherent": [P_f64, c_i32, c_i32, c_i32, c_f64],
     "dare_reslice_device": [c_vp, c_i32, c_vp, c_i32, c_i32, ctypes.POINTER(ResliceCfg), c_vp,
                             c_vp, c_vp],
     "dare_compound": [c_vp, c_i64, c_i32, c_i32, c_i32, P_i32, c_i64, P_f64, c_f64, c_f64, P_u8,

@@ -47,6 +47,7 @@ struct ResliceArgs {
   int tiles_x;
   int brute;           // 1: scan every sample (reslice_rows_bruteforce)
   const int* order;    // launch slot -> pose (spatially sorted batch), or null
+  int pose_major;      // lanes = one pixel of 32 consecutive poses (coherent batches)
   uint32_t n_samples;
 };
 
@@ -132,30 +133,45 @@ constexpr int kSmemBytes = (int)(sizeof(double) * kGateSmem);
 // compulsory 59 MB/pose) and per-lane survivor queues both lost to this
 // version on instruction count or on L1 capacity.
 template <int kDistMode>
-__global__ void __launch_bounds__(256) reslice_k(ResliceArgs a, uint8_t* __restrict__ out,
+__global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                  uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_gate = reinterpret_cast<double*>(smem_raw);
-  const int pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
-  const double* __restrict__ gate_g = a.gate + (size_t)pose * a.n_orient;
-  const bool gate_in_smem = a.n_orient <= kGateSmem;
-  bool gate_filter = true;  // some orientation rejected for this pose -> test it per visit
-  if (gate_in_smem) {
-    bool rej = false;
-    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
-      const double g = gate_g[i];
-      s_gate[i] = g;
-      rej |= g == CUDART_INF;
-    }
-    gate_filter = __syncthreads_or(rej);
-  }
-  const double* gate = gate_in_smem ? s_gate : gate_g;
-
-  const int tile = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = (tile % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
-  const int v = (tile / a.tiles_x) * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const bool active = u < a.W && v < a.H;
+  int pose, u, v;
+  bool active;
+  const double* gate;
+  bool gate_filter = true;  // some orientation rejected for this pose -> test it per visit
+  if (a.pose_major) {
+    // pose-coherent batches (trajectories): lanes = the same pixel in 32
+    // consecutive poses, whose visit streams nearly coincide (broadcast loads);
+    // warps of a block = a 4x2 pixel patch.
+    pose = blockIdx.y * 32 + lane;
+    const int tiles_x4 = (a.W + 3) >> 2;
+    u = (blockIdx.x % tiles_x4) * 4 + (warp & 3);
+    v = (blockIdx.x / tiles_x4) * 2 + (warp >> 2);
+    active = pose < a.P && u < a.W && v < a.H;
+    if (pose >= a.P) pose = a.P - 1;  // inactive lanes read a valid pose
+    gate = a.gate + (size_t)pose * a.n_orient;
+  } else {
+    pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+    const double* __restrict__ gate_g = a.gate + (size_t)pose * a.n_orient;
+    const bool gate_in_smem = a.n_orient <= kGateSmem;
+    if (gate_in_smem) {
+      bool rej = false;
+      for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
+        const double g = gate_g[i];
+        s_gate[i] = g;
+        rej |= g == CUDART_INF;
+      }
+      gate_filter = __syncthreads_or(rej);
+    }
+    gate = gate_in_smem ? s_gate : gate_g;
+    const int tile = blockIdx.x;
+    u = (tile % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
+    v = (tile / a.tiles_x) * 16 + (warp >> 1) * 4 + (lane >> 3);
+    active = u < a.W && v < a.H;
+  }
 
   const double* pp = a.params + (size_t)pose * 14;
   const double du = (double)u * pp[12], dv = (double)v * pp[13];
@@ -285,7 +301,7 @@ __global__ void exp_k(const double* x, double* y, int64_t n) {
 
 static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params, int32_t W,
                            int32_t H, const dare_reslice_cfg* cfg, uint8_t* d_pixels,
-                           uint8_t* d_cov, cudaStream_t s, int brute = 0) {
+                           uint8_t* d_cov, cudaStream_t s, int brute = 0, bool coherent = false) {
   DARE_REQUIRE(vol != nullptr && cfg != nullptr, "null argument");
   DARE_REQUIRE(W > 0 && H > 0, "reslice plane must have at least one pixel");
   DARE_REQUIRE(P >= 0 && P <= 65535, "n_poses must be in [0, 65535] per launch");
@@ -323,8 +339,9 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   }
   pt.mark("gate");
   a.order = nullptr;
+  a.pose_major = (cfg->schedule == 2 || (cfg->schedule == 0 && coherent)) && !brute ? 1 : 0;
   Scratch<int> order(P >= 4 ? P : 0, s);
-  if (P >= 4 && !brute) {
+  if (P >= 4 && !brute && !a.pose_major) {
     Scratch<unsigned long long> keys(2 * (size_t)P, s);
     Scratch<int> idx(P, s);
     pose_key_k<<<ceil_div(P, 128), 128, 0, s>>>(d_params, P, W, H, a.origin[0], a.origin[1],
@@ -338,7 +355,8 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     a.order = order.ptr;
   }
   pt.mark("order");
-  const dim3 grid(a.tiles_x * tiles_y, P);
+  const dim3 grid = a.pose_major ? dim3(ceil_div(W, 4) * ceil_div(H, 2), ceil_div(P, 32))
+                                  : dim3(a.tiles_x * tiles_y, P);
   static bool attr_done = false;  // benign race: idempotent attribute set
   if (!attr_done) {
     DARE_CUDA(cudaFuncSetAttribute(reslice_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -369,6 +387,28 @@ extern "C" int dare_reslice_device(dare_volume_t vol, int32_t n_poses, const dou
   });
 }
 
+// Coherence test for the pose-major schedule (host params).
+static bool poses_coherent(const double* p, int32_t P, int32_t W, int32_t H, double voxel) {
+  if (P < 32) return false;
+  int close = 0;
+  double prev[3] = {0, 0, 0};
+  for (int32_t i = 0; i < P; ++i) {
+    const double* q = p + (size_t)i * 14;
+    const double hu = 0.5 * (W - 1) * q[12], hv = 0.5 * (H - 1) * q[13];
+    const double c[3] = {q[0] + hu * q[3] + hv * q[4], q[1] + hu * q[6] + hv * q[7],
+                         q[2] + hu * q[9] + hv * q[10]};
+    if (i > 0) {
+      const double* o = q - 14;
+      double dr = 0.0;
+      for (int k = 3; k < 12; ++k) dr = fmax(dr, fabs(q[k] - o[k]));
+      const double dc = fmax(fabs(c[0] - prev[0]), fmax(fabs(c[1] - prev[1]), fabs(c[2] - prev[2])));
+      close += (dc <= voxel && dr <= 0.05) ? 1 : 0;
+    }
+    for (int k = 0; k < 3; ++k) prev[k] = c[k];
+  }
+  return close >= (int)(0.9 * (P - 1));
+}
+
 // host-buffer wrapper: params H2D, launches (<= 65535 poses each), outputs D2H
 static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
                          int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
@@ -386,7 +426,8 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
     int32_t np = std::min<int32_t>(65535, n_poses - p0);
     size_t off = (size_t)p0 * width * height;
     launch_reslice(vol, np, d_params.ptr + (size_t)p0 * 14, width, height, cfg, d_out.ptr + off,
-                   d_out.ptr + npix + off, s, brute);
+                   d_out.ptr + npix + off, s, brute,
+                   poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel));
   }
   DARE_CUDA(cudaMemcpyAsync(pixels, d_out.ptr, npix, cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaMemcpyAsync(coverage, d_out.ptr + npix, npix, cudaMemcpyDeviceToHost, s));
@@ -403,6 +444,11 @@ extern "C" int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const
                                        int32_t width, int32_t height, const dare_reslice_cfg* cfg,
                                        uint8_t* pixels, uint8_t* coverage) {
   return guard([&] { reslice_host(vol, n_poses, params, width, height, cfg, pixels, coverage, 1); });
+}
+
+extern "C" int dare_poses_coherent(const double* params, int32_t n_poses, int32_t width,
+                                   int32_t height, double voxel_size) {
+  return poses_coherent(params, n_poses, width, height, voxel_size) ? 1 : 0;
 }
 
 extern "C" int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream) {

@@ -118,10 +118,11 @@ def plane_params(plane) -> tuple[float, ...]:
             float(plane.pixel_pitch[0]), float(plane.pixel_pitch[1]))
 
 
-def kernel_cfg(cfg) -> _lib.ResliceCfg:
+def kernel_cfg(cfg, schedule: int = 0) -> _lib.ResliceCfg:
+    """Kernel scalars; schedule 0 = auto, 1 = pixel-major, 2 = pose-major."""
     return _lib.ResliceCfg(float(cfg.interp_radius), float(cfg.cos_normal_threshold),
                            float(cfg.cos_inplane_threshold), float(cfg.k_normal),
-                           float(cfg.k_inplane), float(cfg.k_dist), int(cfg.unassigned_value), 0)
+                           float(cfg.k_inplane), float(cfg.k_dist), int(cfg.unassigned_value), int(schedule))
 
 
 def _run(fn: str, volume, planes, cfg):

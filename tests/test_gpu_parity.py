@@ -154,6 +154,44 @@ def test_reslice_batch_equals_single_calls(rng):
         np.testing.assert_array_equal(cov[k], one.coverage)
 
 
+def test_pose_major_schedule_identical(rng):
+    """The pose-major schedule (lanes = one pixel of 32 consecutive poses) gives
+    the same bits as the pixel-major one, on a coherent trajectory and on a
+    random batch (forced)."""
+    import ctypes
+
+    from paper_2605_26325_b200 import _lib
+    from paper_2605_26325_b200.reslice import kernel_cfg, plane_params
+
+    vol = _random_volume(rng, 30000, 10.0, 0.25)
+    q0 = Quaternion.from_axis_angle((1, 0.2, 0), 0.3)
+    traj = [ReslicePlane(Pose(Quaternion.from_axis_angle((1, 0.2, 0), 0.3 + 0.002 * k), (2.0 + 0.01 * k, 2.0, 5.0)),
+                         23, 19, (0.2, 0.2)) for k in range(70)]
+    rand = []
+    for _ in range(40):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        rand.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(2, 8, 3)), 23, 19, (0.2, 0.2)))
+    cfg = ResliceConfig(interp_radius=0.25, normal_threshold_deg=60, inplane_threshold_deg=60)
+    handle = vol.device_handle().raw
+    for planes in (traj, rand):
+        params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
+        outs = []
+        for sched in (1, 2):
+            px = np.empty((len(planes), 19, 23), np.uint8)
+            cv = np.empty((len(planes), 19, 23), np.uint8)
+            kc = kernel_cfg(cfg, sched)
+            _lib.call("dare_reslice", handle, len(planes), _lib.ptr(params, ctypes.c_double), 23, 19,
+                      ctypes.byref(kc), _lib.ptr(px, ctypes.c_uint8), _lib.ptr(cv, ctypes.c_uint8))
+            outs.append((px, cv))
+        np.testing.assert_array_equal(outs[0][0], outs[1][0])
+        np.testing.assert_array_equal(outs[0][1], outs[1][1])
+        assert outs[0][1].any()
+    p_traj = np.ascontiguousarray([plane_params(p) for p in traj], dtype=np.float64)
+    assert _lib.load().dare_poses_coherent(_lib.ptr(p_traj, ctypes.c_double), len(traj), 23, 19, 0.25) == 1
+    assert q0 is not None
+
+
 def test_concurrent_reslices_identical(rng):
     vol = _random_volume(rng, 4000)
     plane = ReslicePlane(Pose(Quaternion.identity(), (2.0, 2.0, 5.0)), 24, 20, (0.3, 0.3))
