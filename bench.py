@@ -55,6 +55,7 @@ def parse_args():
     p.add_argument("--config", default="cfg2", choices=sorted(bench_data.CONFIGS))
     p.add_argument("--batch", type=int, default=0, help="poses per step (default: config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-scalar", action="store_true", help="skip the direction-blind arm timings")
     return p.parse_args()
 
 
@@ -257,6 +258,52 @@ def oracle_sample(wl, sweep, plane_list, cfg, gpu=None, patch=None):
             f"{plane_list[0].width}x{plane_list[0].height} planes on a slab-oracle volume (frames within one "
             f"voxel of the plane, full grid){', time scaled by pixel count' if patch else ''}; C+OpenMP")
     return times, parity, what
+
+
+def _best_ms(fn, reps=3):
+    best, out = None, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        ms = (time.perf_counter() - t0) * 1000.0
+        best = ms if best is None else min(best, ms)
+    return best, out
+
+
+def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
+    """Config 5 (direction-blind comparison arm) on the same sweep: compound of
+    the full sweep, fill_holes + trilinear on a sparse variant (every 8th frame,
+    SURVEY §8d) so that gap filling does real work.  Wall time of each C-ABI
+    call (frames in HBM); algorithmic bytes per SURVEY §8d."""
+    from types import SimpleNamespace
+
+    n_in = wl.n_frames * wl.size * wl.size
+    ms_c, sv = _best_ms(lambda: db.compound(dev_sweep, voxel_size=wl.voxel, margin=0.0))
+    ncells = int(np.prod(sv.dims))
+    sparse = SimpleNamespace(images=frames_d[::8].contiguous(), image_timestamps=dev_sweep.image_timestamps[::8],
+                             pose_timestamps=dev_sweep.pose_timestamps[::8], poses=dev_sweep.poses[::8],
+                             pixel_pitch=dev_sweep.pixel_pitch, calibration=dev_sweep.calibration, mask=None)
+    sv_sparse = db.compound(sparse, voxel_size=wl.voxel, margin=0.0)
+    ms_f, filled = _best_ms(lambda: db.fill_holes(sv_sparse, 3))
+    passes = filled.passes_run
+    nc_sparse = int(np.prod(sv_sparse.dims))
+    db.reslice_trilinear_batch(filled, planes)
+    ms_t, _ = _best_ms(lambda: db.reslice_trilinear_batch(filled, planes))
+    hw = planes[0].width * planes[0].height
+    tri_bytes = len(planes) * (8 * hw * 5 + hw * (1 + 1 / 8))  # <= 8 distinct corners per pixel
+    comp_bytes = n_in + ncells * 5
+    fill_bytes = passes * nc_sparse * 10
+    gbs = lambda b, ms: b / (ms / 1000.0) / 1e9  # noqa: E731
+    return {
+        "compound": {"ms": ms_c, "input_Mpix_per_s": n_in / 1e6 / (ms_c / 1000.0),
+                     "algorithmic_GBps": gbs(comp_bytes, ms_c), "frac": gbs(comp_bytes, ms_c) / peak},
+        "fill_holes": {"ms": ms_f, "passes_run": passes, "cells": nc_sparse,
+                       "algorithmic_GBps": gbs(fill_bytes, ms_f) if passes else None,
+                       "sweep": f"every 8th frame ({len(sparse.poses)} frames)"},
+        "trilinear": {"ms_per_batch": ms_t, "poses": len(planes), "reslices_per_s": len(planes) / (ms_t / 1000.0),
+                      "note": "host-buffer C-ABI call incl. pose upload and image download"},
+        "timing": "best of 3 wall-clock C-ABI calls (each synchronises)",
+    }
 
 
 def host_sweep(wl, frames_np):
@@ -487,6 +534,11 @@ def run_b200(args):
     traffic, traffic_src = ncu_traffic(f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>", B, args.config)
     achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
 
+    # ---- direction-blind arm (config 5): compound -> fill_holes -> trilinear ----
+    scalar_arm = None
+    if rank == 0 and not args.no_scalar:
+        scalar_arm = scalar_arm_bench(db, wl, dev_sweep, frames_d, planes[step0 * B:(step0 + 1) * B], peak, torch)
+
     # ---- CPU baseline (rank 0, bounded sample) ----
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -531,6 +583,7 @@ def run_b200(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
             "cpu_baseline": cpu,
+            "scalar_arm": scalar_arm,
         }
         print(json.dumps(out))
     if dist is not None:

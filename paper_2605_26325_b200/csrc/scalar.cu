@@ -32,31 +32,40 @@ struct ScalarFrameView {
   double px, py;
 };
 
+// Same brick decomposition as the reconstruction scatter (csrc/reconstruct.cu):
+// a block keeps a 16(u) x 4(v) pixel tile and strides over groups of 4 frames,
+// each warp covers 8 x 2 x 2 (u, v, frame), so that pixels landing in one cell
+// (image neighbours and consecutive frames) share one pair of atomics.  Integer
+// sums make the result independent of the order (baseline.py:67).
+constexpr int kCBrickU = 16, kCBrickV = 4, kCBrickF = 4;
+
 __global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m,
                                                   unsigned long long* sums,
                                                   unsigned long long* counts) {
-  __shared__ double s_axes[9];
-  const int64_t hw = (int64_t)fv.H * fv.W;
-  const unsigned lane = threadIdx.x & 31u;
-  for (int64_t f = blockIdx.y; f < fv.n_frames; f += gridDim.y) {
-    __syncthreads();
-    if (threadIdx.x < 9) s_axes[threadIdx.x] = fv.axes[f * 9 + threadIdx.x];
-    __syncthreads();
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool valid = p < hw;
-    if (valid && fv.mask) valid = fv.mask[p] != 0;
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t W = (uint32_t)fv.W, H = (uint32_t)fv.H;
+  const uint32_t tiles_u = (W + kCBrickU - 1) / kCBrickU;
+  const uint32_t u = (blockIdx.x % tiles_u) * kCBrickU + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = (blockIdx.x / tiles_u) * kCBrickV + ((warp >> 1) & 1) * 2 + ((lane >> 3) & 1);
+  const uint32_t fl = (warp >> 2) * 2 + (lane >> 4);
+  const uint32_t p = v * W + u;
+  const bool in_frame = u < W && v < H && (!fv.mask || fv.mask[p] != 0);
+  const size_t hw = (size_t)H * W;
+  for (int64_t f0 = (int64_t)blockIdx.y * kCBrickF; f0 < fv.n_frames; f0 += (int64_t)gridDim.y * kCBrickF) {
+    const int64_t f = f0 + fl;
+    const bool valid = in_frame && f < fv.n_frames;
     int64_t lin = -1;
     unsigned inten = 0;
     if (valid) {
       float p32[3];
-      lin = pixel_cell(s_axes, (int)(p % fv.W), (int)(p / fv.W), fv.px, fv.py, m, p32);
+      lin = pixel_cell(fv.axes + f * 9, (int)u, (int)v, fv.px, fv.py, m, p32);
       inten = fv.frames[(size_t)fv.image[f] * hw + p];
     }
-    bool kept = lin >= 0;
-    unsigned active = __ballot_sync(0xffffffffu, kept);
+    const bool kept = lin >= 0;
+    const unsigned active = __ballot_sync(0xffffffffu, kept);
     if (kept) {
-      unsigned peers = __match_any_sync(active, (unsigned long long)lin);
-      unsigned total = __reduce_add_sync(peers, inten);
+      const unsigned peers = __match_any_sync(active, (unsigned long long)lin);
+      const unsigned total = __reduce_add_sync(peers, inten);
       if (lane == (unsigned)(__ffs(peers) - 1)) {
         atomicAdd(&sums[lin], (unsigned long long)total);
         atomicAdd(&counts[lin], (unsigned long long)__popc(peers));
@@ -88,46 +97,71 @@ __global__ void to_f64_k(int64_t n, const float* __restrict__ v, double* w) {
 // known in pass p: observed (1), filled earlier (2 or a tag from pass < p)
 __device__ __forceinline__ bool known_in_pass(uint8_t f, int tag) { return f != 0 && f != tag; }
 
+// One Jacobi pass, tiled: a block owns a 4(x) x 8(y) x 32(z) brick (thread =
+// one (y, z) line of 4 x-cells, z fastest -> coalesced), stages the brick plus
+// a one-cell halo as (known ? value : 0, known) in shared memory, and every
+// empty cell sums its 26 neighbours in C order from there.  In place: a cell
+// filled in this pass carries `tag` and reads as unknown to every reader of
+// this pass, whether it sees the old or the new flag (Jacobi semantics).
+constexpr int kFX = 4, kFY = 8, kFZ = 32;
+constexpr int kHX = kFX + 2, kHY = kFY + 2, kHZ = kFZ + 2;
+
 __global__ void __launch_bounds__(256) fill_pass_k(int64_t nx, int64_t ny, int64_t nz,
                                                    double* v, uint8_t* flags, int tag,
                                                    unsigned long long* filled,
                                                    const unsigned long long* prev_filled) {
   if (prev_filled && *prev_filled == 0) return;  // previous pass changed nothing
-  const int64_t n = nx * ny * nz;
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool did = false;
-  if (c < n && flags[c] == 0) {
-    const int64_t z = c % nz, y = (c / nz) % ny, x = c / (ny * nz);
-    double s = 0.0, cnt = 0.0;
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int64_t X = x + dx;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int64_t Y = y + dy;
-        for (int dz = -1; dz <= 1; ++dz) {
-          if (dx == 0 && dy == 0 && dz == 0) continue;
-          const int64_t Z = z + dz;
-          double val = 0.0, k = 0.0;
-          if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
-            const int64_t q = (X * ny + Y) * nz + Z;
-            const uint8_t fq = ((volatile uint8_t*)flags)[q];
-            if (known_in_pass(fq, tag)) {
-              val = v[q];
-              k = 1.0;
-            }
-          }
-          s += val;
-          cnt += k;
-        }
+  __shared__ double s_val[kHX * kHY * kHZ];
+  __shared__ uint8_t s_known[kHX * kHY * kHZ];
+  const int64_t bz = (nz + kFZ - 1) / kFZ, by = (ny + kFY - 1) / kFY;
+  const int64_t b = blockIdx.x;
+  const int64_t z0 = (b % bz) * kFZ, y0 = ((b / bz) % by) * kFY, x0 = (b / (bz * by)) * kFX;
+  const int tz = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t y = y0 + ty, z = z0 + tz;
+  bool empty_here = false;
+  for (int i = 0; i < kFX; ++i) {
+    const int64_t x = x0 + i;
+    if (x < nx && y < ny && z < nz) empty_here |= flags[(x * ny + y) * nz + z] == 0;
+  }
+  if (!__syncthreads_or(empty_here)) return;  // nothing to fill in this brick
+  for (int e = threadIdx.x; e < kHX * kHY * kHZ; e += blockDim.x) {
+    const int hz = e % kHZ, hy = (e / kHZ) % kHY, hx = e / (kHZ * kHY);
+    const int64_t X = x0 + hx - 1, Y = y0 + hy - 1, Z = z0 + hz - 1;
+    double val = 0.0;
+    uint8_t kn = 0;
+    if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
+      const int64_t q = (X * ny + Y) * nz + Z;
+      if (known_in_pass(((volatile uint8_t*)flags)[q], tag)) {
+        val = v[q];
+        kn = 1;
       }
     }
+    s_val[e] = val;
+    s_known[e] = kn;
+  }
+  __syncthreads();
+  bool did = false;
+  for (int i = 0; i < kFX; ++i) {
+    const int64_t x = x0 + i;
+    if (x >= nx || y >= ny || z >= nz) continue;
+    const int64_t c = (x * ny + y) * nz + z;
+    if (flags[c] != 0) continue;
+    double s = 0.0, cnt = 0.0;
+    for (int dx = 0; dx < 3; ++dx)
+      for (int dy = 0; dy < 3; ++dy)
+        for (int dz = 0; dz < 3; ++dz) {
+          if (dx == 1 && dy == 1 && dz == 1) continue;
+          const int e = ((i + dx) * kHY + (ty + dy)) * kHZ + (tz + dz);
+          s += s_val[e];
+          cnt += (double)s_known[e];
+        }
     if (cnt > 0.0) {
       v[c] = s / cnt;
       flags[c] = (uint8_t)tag;
       did = true;
     }
   }
-  int any = __syncthreads_or(did);
-  if (threadIdx.x == 0 && any) atomicAdd(filled, 1ull);
+  if (__syncthreads_or(did) && threadIdx.x == 0) atomicAdd(filled, 1ull);
 }
 
 __global__ void fill_finalize_k(int64_t n, const double* __restrict__ v, const uint8_t* flags_in,
@@ -274,7 +308,9 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
                        fs.H,        fs.W,       fs.px,     fs.py};
     const int64_t hw = (int64_t)height * width;
     if (n_frames > 0) {
-      dim3 grid(ceil_div(hw, 256), (unsigned)std::min<int64_t>(n_frames, 65535));
+      (void)hw;
+      dim3 grid(ceil_div(width, kCBrickU) * ceil_div(height, kCBrickV),
+                (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n_frames, kCBrickF), 1), 8));
       compound_k<<<grid, 256, 0, s>>>(fv, m, (unsigned long long*)d_sums,
                                       (unsigned long long*)d_counts);
       DARE_CUDA(cudaGetLastError());
@@ -393,7 +429,9 @@ extern "C" int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar
     DARE_CUDA(cudaMemcpyAsync(flags.ptr, in->d_flags, n, cudaMemcpyDeviceToDevice, s));
     to_f64_k<<<ceil_div(n, 256), 256, 0, s>>>(n, in->d_values, work.ptr);
     for (int p = 0; p < max_passes; ++p) {
-      fill_pass_k<<<ceil_div(n, 256), 256, 0, s>>>(in->dims[0], in->dims[1], in->dims[2],
+      const unsigned fill_blocks = ceil_div(in->dims[0], kFX) * ceil_div(in->dims[1], kFY) *
+                                   ceil_div(in->dims[2], kFZ);
+      fill_pass_k<<<fill_blocks, 256, 0, s>>>(in->dims[0], in->dims[1], in->dims[2],
                                                     work.ptr, flags.ptr, 3 + p, filled.ptr + p,
                                                     p ? filled.ptr + p - 1 : nullptr);
       DARE_CUDA(cudaGetLastError());
