@@ -177,16 +177,15 @@ def test_pose_major_schedule_identical(rng):
     for planes in (traj, rand):
         params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
         outs = []
-        for sched in (1, 2, 3):
+        for sched in (1, 2):
             px = np.empty((len(planes), 19, 23), np.uint8)
             cv = np.empty((len(planes), 19, 23), np.uint8)
             kc = kernel_cfg(cfg, sched)
             _lib.call("dare_reslice", handle, len(planes), _lib.ptr(params, ctypes.c_double), 23, 19,
                       ctypes.byref(kc), _lib.ptr(px, ctypes.c_uint8), _lib.ptr(cv, ctypes.c_uint8))
             outs.append((px, cv))
-        for o in outs[1:]:
-            np.testing.assert_array_equal(outs[0][0], o[0])
-            np.testing.assert_array_equal(outs[0][1], o[1])
+        np.testing.assert_array_equal(outs[0][0], outs[1][0])
+        np.testing.assert_array_equal(outs[0][1], outs[1][1])
         assert outs[0][1].any()
     p_traj = np.ascontiguousarray([plane_params(p) for p in traj], dtype=np.float64)
     assert _lib.load().dare_poses_coherent(_lib.ptr(p_traj, ctypes.c_double), len(traj), 23, 19, 0.25) == 1
