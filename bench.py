@@ -56,6 +56,8 @@ def parse_args():
     p.add_argument("--batch", type=int, default=0, help="poses per step (default: config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-scalar", action="store_true", help="skip the direction-blind arm timings")
+    p.add_argument("--exact", action="store_true",
+                   help="FP64 reference arithmetic for every pixel (default: certified f32 + exact fallback)")
     return p.parse_args()
 
 
@@ -459,7 +461,7 @@ def run_b200(args):
     coherent = _lib.load().dare_poses_coherent(p0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B, W, H,
                                                float(wl.voxel))
     schedule = 2 if coherent else 1
-    kc = kernel_cfg(cfg, schedule)
+    kc = kernel_cfg(cfg, schedule, exact=args.exact)
     # a real (non-default) stream: the kernels and the timing events share it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -507,6 +509,10 @@ def run_b200(args):
         host_call(args.warmup + s)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = ws * B * args.steps / e2e_s
+    fb = ctypes.c_int64()
+    _lib.call("dare_reslice_last_fallback", ctypes.byref(fb))
+    certified = {"path": "exact" if args.exact else "certified f32 + exact fallback",
+                 "fallback_pixels_last_step": int(fb.value), "fallback_fraction": fb.value / (B * H * W)}
 
     # ---- p50 single-pose latency through the public API ----
     lat = []
@@ -531,7 +537,14 @@ def run_b200(args):
         ref_bytes += 12 * len(cells) + 29 * float(c.sum().item()) + H * W * (1 + 1 / 8)
         own_bytes += 4 * len(cells) + 16 * float(c.sum().item()) + H * W * 2
     peak, peak_kind = hbm_peak()
-    traffic, traffic_src = ncu_traffic(f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>", B, args.config)
+    if args.exact:
+        main_kernel = f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>"
+    else:
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}>"
+    traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
+    # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
+    # [fallback kernel on the certified path]
+    launches_per_step = 2 + (2 if schedule == 1 and B >= 4 else 0) + (0 if args.exact else 1)
     achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
 
     # ---- direction-blind arm (config 5): compound -> fill_holes -> trilinear ----
@@ -576,11 +589,12 @@ def run_b200(args):
                     "d2h_bytes_per_step": 2 * B * H * W},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "reslice_k (+gate_k)",
+                         "kernel": main_kernel,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_step_ref_layout": ref_bytes,
                          "compulsory_bytes_per_step_own_layout": own_bytes},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
+            "certified": certified,
             "clocks": clk,
             "cpu_baseline": cpu,
             "scalar_arm": scalar_arm,

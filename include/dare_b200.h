@@ -65,6 +65,11 @@ typedef struct {
   int32_t schedule; /* 0 auto, 1 pixel-major (spatially sorted batch), 2 pose-major
                        (lanes = one pixel of 32 consecutive poses; for coherent
                        trajectories).  Results are identical; only speed differs. */
+  int32_t exact;    /* 0: certified f32 weights with exact-FP64 fallback for every
+                       pixel whose u8 value / coverage the error bound cannot decide
+                       (default); 1: FP64 reference arithmetic for every pixel.
+                       Both produce the reference's pixels bit-for-bit. */
+  int32_t _pad;
 } dare_reslice_cfg;
 
 typedef struct {
@@ -231,6 +236,16 @@ int dare_reslice_trilinear_device(dare_scalar_t vol, int32_t n_poses, const doub
 /* ---- diagnostics -------------------------------------------------------- */
 /* Device restatement of glibc exp on n device doubles (parity tests). */
 int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream);
+/* Pixels the last dare_reslice / dare_reslice_bruteforce call on this thread
+ * recomputed on the exact FP64 path because the certified bound was
+ * inconclusive (0 with cfg.exact = 1, or when the fast path is disabled). */
+int dare_reslice_last_fallback(int64_t* n_pixels);
+/* Exhaustive check (every f32 input of the ranges the certified reslice path
+ * uses) of the hardware ex2.approx / rsqrt.approx relative error on the
+ * current device; *ok = 1 when both are within the constants the bound
+ * assumes.  The fast path runs this once per device and disables itself
+ * (exact FP64 for every pixel) if it fails. */
+int dare_fastmath_check(double* ex2_max_rel_err, double* rsqrt_max_rel_err, int32_t* ok);
 
 #ifdef __cplusplus
 }

@@ -40,7 +40,7 @@ class ResliceCfg(ctypes.Structure):
     _fields_ = [
         ("radius", c_f64), ("cos_normal", c_f64), ("cos_inplane", c_f64),
         ("k_normal", c_f64), ("k_inplane", c_f64), ("k_dist", c_f64),
-        ("unassigned", c_i32), ("schedule", c_i32),
+        ("unassigned", c_i32), ("schedule", c_i32), ("exact", c_i32), ("_pad", c_i32),
     ]
 
 
@@ -103,6 +103,8 @@ _SIGNATURES = {
     "dare_reslice_trilinear": [c_vp, c_i32, P_f64, c_i32, c_i32, P_u8, P_u8, P_f64],
     "dare_reslice_trilinear_device": [c_vp, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp],
     "dare_exp_device": [c_vp, c_vp, c_i64, c_vp],
+    "dare_reslice_last_fallback": [P_i64],
+    "dare_fastmath_check": [P_f64, P_f64, P_i32],
 }
 
 EXPORTED = ["dare_last_error", *_SIGNATURES]

@@ -4,22 +4,35 @@
 // (_kernels.py:84-139) -> _accumulate_run (29-68) -> _finalize_pixel (71-81).
 //
 // Per pixel the reference walks the clamped cell range x -> y -> z ascending
-// and, per cell, its run in storage order, accumulating wsum / iwsum in FP64.
-// That order is kept exactly (thread per pixel, same walk), so every pixel is
-// bit-identical.  What changes is where the work goes:
+// and, per cell, its run in storage order, accumulating wsum / iwsum in FP64,
+// then emits floor(iwsum / wsum + 0.5) (clamped to u8) when wsum >= 1e-12.
+// Two device paths produce that u8 bit-for-bit:
+//
+// * exact (reslice_k): the reference's FP64 arithmetic restated in the same
+//   order per pixel (thread per pixel, same walk);
+// * certified (reslice_fast_k, default): the SAME survivor set (exact cube and
+//   gate tests), but each weight is evaluated in f32 with the hardware ex2 /
+//   rsqrt approximations and the sums carry a rigorous relative error bound
+//   (derivation at certify()).  Because the output is a rounded u8 and a
+//   threshold test, the bound decides the reference's result for all but a
+//   tiny fraction of pixels; those are appended to a list and recomputed by
+//   the exact path (reslice_fallback_k).  The MUFU error constants the bound
+//   assumes are verified exhaustively on the device before first use.
+//
+// Shared restructuring (both paths):
 //   * orientation gates and the orientation exponent
 //       A = k_n (d_n - 1) + k_i (d_i - 1)                  (_kernels.py:47-65)
 //     depend only on (pose, sample quaternion); they are evaluated once per
-//     (pose, distinct orientation) by gate_k, bit-identically, and the walk
-//     reads one double per visit instead of redoing 30 FP64 ops;
-//   * because rejection is a pure filter, the gate is tested before the cube
-//     (same survivors, same order);
+//     (pose, distinct orientation) by gate_k, bit-identically;
+//   * rejection is a pure filter, so the gate is tested with the cube (same
+//     survivors, same order);
 //   * for fixed (cx, cy) the cells loz..hiz are adjacent in the CSR, so their
 //     runs form ONE contiguous sample range [off[base+loz], off[base+hiz+1]);
-//   * (k_d * dist) / r uses an exact reciprocal multiply when r is a power of
-//     two, and is skipped entirely when k_d == 0 (the term is exactly +0.0);
-//   * exp is the bit-exact glibc port (dare_exp.h).
+//   * exact path: (k_d * dist) / r uses an exact reciprocal multiply when r is
+//     a power of two, skipped when k_d == 0; exp is the glibc port (dare_exp.h).
 #include <math_constants.h>
+
+#include <mutex>
 
 #include "dare_exp.h"
 #include <cub/device/device_radix_sort.cuh>
@@ -30,17 +43,29 @@ namespace dare {
 
 constexpr double kCoverageMinWeight = 1e-12;  // _kernels.py:20
 constexpr double kCellRangeGuard = 1e-9;      // _kernels.py:26
+constexpr double kLog2e = 1.4426950408889634;
+constexpr double kLn2 = 0.6931471805599453;
+constexpr double kEps32 = 5.9604644775390625e-08;   // 2^-24, f32 unit roundoff
+constexpr double kEps64 = 1.1102230246251565e-16;   // 2^-53
+// Relative-error constants the certified bound assumes for the hardware
+// approximations; dare_fastmath_check verifies them exhaustively per device.
+constexpr double kEx2Err = 4.76837158203125e-07;    // 2^-21
+constexpr double kRsqErr = 4.76837158203125e-07;    // 2^-21
+constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fast path accepts
 
 struct ResliceArgs {
   const uint32_t* offsets;
   const uint4* records;
   const double* params;  // P x 14
   const double* gate;    // P x n_orient (A, or +inf when rejected)
+  const float* gate2;    // P x n_orient: f32(A * log2 e), +inf when rejected
   int64_t n_orient;
   double origin[3];
   double voxel;
   int64_t dims[3];
   double radius, inv_radius, kd;
+  float c2;              // f32(k_d * log2 e / r)
+  double lam;            // per-term |ln(w_fast / w_ref)| bound, position term excluded
   int dist_mode;  // 0: divide, 1: exact reciprocal, 2: k_d == 0
   int unassigned;
   int W, H, P;
@@ -49,12 +74,17 @@ struct ResliceArgs {
   const int* order;    // launch slot -> pose (spatially sorted batch), or null
   int pose_major;      // lanes = one pixel of 32 consecutive poses (coherent batches)
   uint32_t n_samples;
+  unsigned long long* amb;   // certified path: pixels left to the exact path
+  unsigned* amb_count;
+  unsigned amb_cap;
+  unsigned long long* fallback_total;  // optional running count (stats)
 };
 
-// gate table: one thread per (orientation, pose)
+// gate table: one thread per (orientation, pose); the certified path's f32
+// copy is pre-scaled to log2 units.
 __global__ void gate_k(const float4* __restrict__ orient, int64_t n_orient,
                        const double* __restrict__ params, int P, dare_reslice_cfg cfg,
-                       double* gate) {
+                       double* gate, float* gate2) {
   int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int p = blockIdx.y;
   if (o >= n_orient || p >= P) return;
@@ -76,6 +106,7 @@ __global__ void gate_k(const float4* __restrict__ orient, int64_t n_orient,
     if (!(di < cfg.cos_inplane)) A = cfg.k_normal * (dn - 1.0) + cfg.k_inplane * (di - 1.0);
   }
   gate[(size_t)p * n_orient + o] = A;
+  gate2[(size_t)p * n_orient + o] = __double2float_rn(A * kLog2e);
 }
 
 __device__ __forceinline__ void cell_range(double w, double r, double o, double inv_v, int64_t n,
@@ -117,82 +148,73 @@ __device__ __forceinline__ float keep_lo(double w, double r) {
   return p;
 }
 
-constexpr int kGateSmem = 512;  // orientation table entries staged in shared memory
-constexpr int kSmemBytes = (int)(sizeof(double) * kGateSmem);
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
-// 256 threads = one 16x16 pixel tile; each warp covers 8x4 pixels; thread per
-// pixel, walking its cell columns in the reference order.  Per-visit work is
-// an exact f32 interval test (keep_lo/keep_hi) plus, when this pose rejects
-// any orientation, the gate lookup; survivors get the FP64 weight.  To keep
-// the FP64 path converged, the warp advances in rounds: every lane scans
-// forward to its next survivor (cheap, divergent), then all lanes that found
-// one evaluate it together.
-//
-// Measured alternatives (profiles/round1_reslice_variants.md): warp-
-// cooperative run scans with per-pixel survivor rows (coalesced, DRAM at the
-// compulsory 59 MB/pose) and per-lane survivor queues both lost to this
-// version on instruction count or on L1 capacity.
-template <int kDistMode>
-__global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __restrict__ out,
-                                                 uint8_t* __restrict__ cov) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s_gate = reinterpret_cast<double*>(smem_raw);
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+constexpr int kSmemBytes = 4096;                        // gate table staged in shared memory
+constexpr int kGateSmem = kSmemBytes / sizeof(double);  // exact path (f64 entries)
+constexpr int kGateSmemF = kSmemBytes / sizeof(float);  // certified path (f32 entries)
+
+// Launch mapping.  Pixel-major: 256 threads = one 16x16 pixel tile of one pose
+// (warp = 8x4 pixels).  Pose-major (coherent batches, e.g. trajectories):
+// lanes = the same pixel in 32 consecutive poses, whose visit streams nearly
+// coincide (broadcast loads); warps of a block = a 4x2 pixel patch.
+__device__ __forceinline__ void map_pixel(const ResliceArgs& a, int& pose, int& u, int& v,
+                                          bool& active) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int pose, u, v;
-  bool active;
-  const double* gate;
-  bool gate_filter = true;  // some orientation rejected for this pose -> test it per visit
   if (a.pose_major) {
-    // pose-coherent batches (trajectories): lanes = the same pixel in 32
-    // consecutive poses, whose visit streams nearly coincide (broadcast loads);
-    // warps of a block = a 4x2 pixel patch.
     pose = blockIdx.y * 32 + lane;
     const int tiles_x4 = (a.W + 3) >> 2;
     u = (blockIdx.x % tiles_x4) * 4 + (warp & 3);
     v = (blockIdx.x / tiles_x4) * 2 + (warp >> 2);
     active = pose < a.P && u < a.W && v < a.H;
     if (pose >= a.P) pose = a.P - 1;  // inactive lanes read a valid pose
-    gate = a.gate + (size_t)pose * a.n_orient;
   } else {
     pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
-    const double* __restrict__ gate_g = a.gate + (size_t)pose * a.n_orient;
-    const bool gate_in_smem = a.n_orient <= kGateSmem;
-    if (gate_in_smem) {
-      bool rej = false;
-      for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
-        const double g = gate_g[i];
-        s_gate[i] = g;
-        rej |= g == CUDART_INF;
-      }
-      gate_filter = __syncthreads_or(rej);
-    }
-    gate = gate_in_smem ? s_gate : gate_g;
     const int tile = blockIdx.x;
     u = (tile % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
     v = (tile / a.tiles_x) * 16 + (warp >> 1) * 4 + (lane >> 3);
     active = u < a.W && v < a.H;
   }
+}
 
-  const double* pp = a.params + (size_t)pose * 14;
-  const double du = (double)u * pp[12], dv = (double)v * pp[13];
-  const double wx = (pp[0] + du * pp[3]) + dv * pp[4];
-  const double wy = (pp[1] + du * pp[6]) + dv * pp[7];
-  const double wz = (pp[2] + du * pp[9]) + dv * pp[10];
-  const double r = a.radius;
-  const double inv_v = 1.0 / a.voxel;
-  int64_t lox, hix, loy, hiy, loz, hiz;
-  cell_range(wx, r, a.origin[0], inv_v, a.dims[0], lox, hix);
-  cell_range(wy, r, a.origin[1], inv_v, a.dims[1], loy, hiy);
-  cell_range(wz, r, a.origin[2], inv_v, a.dims[2], loz, hiz);
-  const float xlo = keep_lo(wx, r), xhi = keep_hi(wx, r);
-  const float ylo = keep_lo(wy, r), yhi = keep_hi(wy, r);
-  const float zlo = keep_lo(wz, r), zhi = keep_hi(wz, r);
+// Pixel-major blocks share one pose: stage its gate row in shared memory.
+// Returns the row to read and whether any orientation is rejected.
+template <class G, int kCap>
+__device__ __forceinline__ const G* stage_gate(const ResliceArgs& a, const G* gate_g, G* s_gate,
+                                               bool& any_rejected) {
+  any_rejected = true;
+  if (a.pose_major || a.n_orient > kCap) return gate_g;
+  bool rej = false;
+  for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
+    const G g = gate_g[i];
+    s_gate[i] = g;
+    rej |= !(g < (G)CUDART_INF);
+  }
+  any_rejected = __syncthreads_or(rej);
+  return s_gate;
+}
 
-  // run cursor over the (cx, cy) columns; each column's cells loz..hiz are one
-  // contiguous sample range [off[base+loz], off[base+hiz+1])
-  int64_t cx = lox, cy = loy;
-  uint32_t s = 0, e = 0;
-  auto open_run = [&]() -> bool {
+// One pixel's walk over its cell columns, in the reference order: cursor over
+// the (cx, cy) columns; each column's cells loz..hiz are one contiguous sample
+// range [off[base+loz], off[base+hiz+1]).
+struct Walk {
+  double wx, wy, wz;
+  float xlo, xhi, ylo, yhi, zlo, zhi;
+  int64_t lox, hix, loy, hiy, loz, hiz, cx, cy;
+  uint32_t s, e;
+  bool live;
+
+  __device__ __forceinline__ bool open_run(const ResliceArgs& a) {
     if (a.brute) {
       if (cx > lox) return false;
       s = 0;
@@ -211,55 +233,168 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
       if (s < e) return true;
     }
     return false;
-  };
-  bool live = active && (a.brute ? true : (lox <= hix && loy <= hiy && loz <= hiz)) && open_run();
-  auto keep = [&](const uint4& c) -> bool {
-    const float x = __uint_as_float(c.x), y = __uint_as_float(c.y), z = __uint_as_float(c.z);
-    return x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi &&
-           (!gate_filter || gate[c.w >> 8] != CUDART_INF);
-  };
+  }
 
-  // Each lane holds a batch of up to 4 consecutive records of its current run
-  // (4 independent loads in flight) and a bit mask of the batch's survivors.
-  // Rounds: lanes with an exhausted batch refill (cheap, divergent); then
-  // every lane with a pending survivor evaluates it (converged FP64 path).
+  // Certified path: the sums are order-independent (the bound does not depend
+  // on the order), so columns are visited in phases (cx mod 3, cy mod 3):
+  // within a phase, the 3x3 neighbouring pixels that share a column read it
+  // together (same addresses in the same warp instruction) instead of a third
+  // of the walk apart, which is what kept the column out of L1/L2 between its
+  // readers.  jx/jy are the phase; every column of the range is visited once.
+  __device__ __forceinline__ bool open_run_phased(const ResliceArgs& a, int& jx, int& jy) {
+    while (jx < 3) {
+      while (cx <= hix) {
+        const int64_t base0 = cx * a.dims[1];
+        while (cy <= hiy) {
+          const int64_t base = (base0 + cy) * a.dims[2];
+          s = __ldg(a.offsets + base + loz);
+          e = __ldg(a.offsets + base + hiz + 1);
+          cy += 3;
+          if (s < e) return true;
+        }
+        cx += 3;
+        cy = loy + (jy - loy % 3 + 3) % 3;
+      }
+      if (++jy == 3) {
+        jy = 0;
+        ++jx;
+      }
+      cx = lox + (jx - lox % 3 + 3) % 3;
+      cy = loy + (jy - loy % 3 + 3) % 3;
+    }
+    return false;
+  }
+
+  __device__ __forceinline__ bool in_cube(const uint4& c) const {
+    const float x = __uint_as_float(c.x), y = __uint_as_float(c.y), z = __uint_as_float(c.z);
+    return x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi;
+  }
+
+  __device__ __forceinline__ void init(const ResliceArgs& a, int pose, int u, int v, bool active,
+                                       bool phased = false) {
+    const double* pp = a.params + (size_t)pose * 14;
+    const double du = (double)u * pp[12], dv = (double)v * pp[13];
+    wx = (pp[0] + du * pp[3]) + dv * pp[4];
+    wy = (pp[1] + du * pp[6]) + dv * pp[7];
+    wz = (pp[2] + du * pp[9]) + dv * pp[10];
+    const double r = a.radius;
+    const double inv_v = 1.0 / a.voxel;
+    cell_range(wx, r, a.origin[0], inv_v, a.dims[0], lox, hix);
+    cell_range(wy, r, a.origin[1], inv_v, a.dims[1], loy, hiy);
+    cell_range(wz, r, a.origin[2], inv_v, a.dims[2], loz, hiz);
+    xlo = keep_lo(wx, r), xhi = keep_hi(wx, r);
+    ylo = keep_lo(wy, r), yhi = keep_hi(wy, r);
+    zlo = keep_lo(wz, r), zhi = keep_hi(wz, r);
+    s = e = 0;
+    const bool nonempty = a.brute ? true : (lox <= hix && loy <= hiy && loz <= hiz);
+    if (phased) {  // phase (0, 0): first column with cx = cy = 0 (mod 3); caller opens
+      cx = lox + (3 - lox % 3) % 3;
+      cy = loy + (3 - loy % 3) % 3;
+      live = active && nonempty;
+    } else {
+      cx = lox;
+      cy = loy;
+      live = active && nonempty && open_run(a);
+    }
+  }
+};
+
+// The reference's FP64 weight of one survivor (_kernels.py:47-68).
+template <int kDistMode>
+__device__ __forceinline__ double exact_weight(const ResliceArgs& a, const Walk& w, const uint4& c,
+                                               const double* gate) {
+  const double dx = (double)__uint_as_float(c.x) - w.wx;
+  const double dy = (double)__uint_as_float(c.y) - w.wy;
+  const double dz = (double)__uint_as_float(c.z) - w.wz;
+  double arg = gate[c.w >> 8];
+  if (kDistMode != 2) {
+    const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+    const double kdd = a.kd * dist;
+    arg = arg - (kDistMode == 1 ? kdd * a.inv_radius : kdd / a.radius);
+  }
+  return dare_exp(arg);
+}
+
+// Exact FP64 sums in the reference order.  Each lane holds a batch of up to 4
+// consecutive records of its current run (4 independent loads in flight) and
+// a bit mask of the batch's survivors.  Rounds: lanes with an exhausted batch
+// refill (cheap, divergent); then every lane with a pending survivor
+// evaluates it (converged FP64 path).  Warp-collective: all 32 lanes call it.
+template <int kDistMode>
+__device__ __forceinline__ void exact_sums(Walk& w, const ResliceArgs& a, const double* gate,
+                                           bool gate_filter, double& wsum, double& iwsum) {
+  auto keep = [&](const uint4& c) -> bool {
+    return w.in_cube(c) && (!gate_filter || gate[c.w >> 8] != CUDART_INF);
+  };
   uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
   unsigned mask = 0;
-  double wsum = 0.0, iwsum = 0.0;
+  wsum = 0.0;
+  iwsum = 0.0;
   while (true) {
-    while (live && mask == 0) {
-      const uint32_t n = min(4u, e - s);
-      const uint4* __restrict__ q = a.records + s;
+    while (w.live && mask == 0) {
+      const uint32_t n = min(4u, w.e - w.s);
+      const uint4* __restrict__ q = a.records + w.s;
       r0 = __ldg(q);
       if (n > 1) r1 = __ldg(q + 1);
       if (n > 2) r2 = __ldg(q + 2);
       if (n > 3) r3 = __ldg(q + 3);
-      s += n;
+      w.s += n;
       mask = (keep(r0) ? 1u : 0u) | ((n > 1 && keep(r1)) ? 2u : 0u) | ((n > 2 && keep(r2)) ? 4u : 0u) |
              ((n > 3 && keep(r3)) ? 8u : 0u);
-      if (s == e) live = open_run();
+      if (w.s == w.e) w.live = w.open_run(a);
     }
     if (!__any_sync(0xffffffffu, mask != 0)) break;
     if (mask) {
       const unsigned kk = __ffs(mask) - 1;
       mask &= mask - 1;
       const uint4 cur = kk == 0 ? r0 : (kk == 1 ? r1 : (kk == 2 ? r2 : r3));
-      const double dx = (double)__uint_as_float(cur.x) - wx;
-      const double dy = (double)__uint_as_float(cur.y) - wy;
-      const double dz = (double)__uint_as_float(cur.z) - wz;
-      double arg = gate[cur.w >> 8];
-      if (kDistMode != 2) {
-        const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
-        const double kdd = a.kd * dist;
-        arg = arg - (kDistMode == 1 ? kdd * a.inv_radius : kdd / r);
-      }
-      const double w = dare_exp(arg);
-      wsum += w;
-      iwsum += w * (double)(cur.w & 0xffu);
+      const double wt = exact_weight<kDistMode>(a, w, cur, gate);
+      wsum += wt;
+      iwsum += wt * (double)(cur.w & 0xffu);
     }
   }
-  if (!active) return;
-  const size_t k = ((size_t)pose * a.H + v) * a.W + u;
+}
+
+// Warp-cooperative exact sums for ONE pixel (all lanes hold the same walk):
+// lanes load 32 consecutive records of the run (coalesced), test and weigh
+// them in parallel, then the survivors are added in storage order through
+// shuffles -- the same sequence of FP64 additions as the reference, with the
+// exp latency overlapped across lanes instead of serialised.
+template <int kDistMode>
+__device__ __forceinline__ void exact_sums_warp(Walk& w, const ResliceArgs& a, const double* gate,
+                                                double& wsum, double& iwsum) {
+  const int lane = threadIdx.x & 31;
+  wsum = 0.0;
+  iwsum = 0.0;
+  while (w.live) {
+    for (uint32_t b = w.s; b < w.e; b += 32) {
+      const uint32_t i = b + lane;
+      bool k = false;
+      double wt = 0.0, wi = 0.0;
+      if (i < w.e) {
+        const uint4 c = __ldg(a.records + i);
+        k = w.in_cube(c) && gate[c.w >> 8] != CUDART_INF;
+        if (k) {
+          wt = exact_weight<kDistMode>(a, w, c, gate);
+          wi = wt * (double)(c.w & 0xffu);
+        }
+      }
+      unsigned m = __ballot_sync(0xffffffffu, k);
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        wsum += __shfl_sync(0xffffffffu, wt, l);
+        iwsum += __shfl_sync(0xffffffffu, wi, l);
+      }
+    }
+    w.s = w.e;
+    w.live = w.open_run(a);
+  }
+}
+
+// _finalize_pixel (_kernels.py:71-81)
+__device__ __forceinline__ void write_exact(const ResliceArgs& a, size_t k, double wsum,
+                                            double iwsum, uint8_t* out, uint8_t* cov) {
   if (wsum >= kCoverageMinWeight) {
     double f = floor(iwsum / wsum + 0.5);
     f = f < 0.0 ? 0.0 : (f > 255.0 ? 255.0 : f);
@@ -268,6 +403,172 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
   } else {
     out[k] = (uint8_t)a.unassigned;
     cov[k] = 0;
+  }
+}
+
+// Exact path: thread per pixel; per-visit work is the exact f32 interval test
+// plus, when this pose rejects any orientation, the gate lookup; survivors get
+// the FP64 weight.  Measured alternatives: profiles/round1_reslice_variants.md.
+template <int kDistMode>
+__global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __restrict__ out,
+                                                 uint8_t* __restrict__ cov) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int pose, u, v;
+  bool active;
+  map_pixel(a, pose, u, v, active);
+  bool gate_filter;
+  const double* gate = stage_gate<double, kGateSmem>(a, a.gate + (size_t)pose * a.n_orient,
+                                                     reinterpret_cast<double*>(smem_raw), gate_filter);
+  Walk w;
+  w.init(a, pose, u, v, active);
+  double wsum, iwsum;
+  exact_sums<kDistMode>(w, a, gate, gate_filter, wsum, iwsum);
+  if (active) write_exact(a, ((size_t)pose * a.H + v) * a.W + u, wsum, iwsum, out, cov);
+}
+
+// One visited record on the certified path: exact survivor test, f32 weight
+// 2^(A2 - dist * c2) (0 for non-survivors), accumulated into the batch sums.
+template <int kDistMode>
+__device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Walk& w,
+                                          const float* gate, const float (&wh)[3],
+                                          const float (&wl)[3], float c2, float& bw, float& bj) {
+  const float g = gate[c.w >> 8];
+  const bool k = valid && w.in_cube(c) && g != CUDART_INF_F;
+  float arg = g;
+  if (kDistMode != 2) {
+    const float dx = __fsub_rn(__fsub_rn(__uint_as_float(c.x), wh[0]), wl[0]);
+    const float dy = __fsub_rn(__fsub_rn(__uint_as_float(c.y), wh[1]), wl[1]);
+    const float dz = __fsub_rn(__fsub_rn(__uint_as_float(c.z), wh[2]), wl[2]);
+    const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    const float dist = __fmul_rn(d2, rsqrt_approx(fmaxf(d2, 1e-30f)));
+    arg = __fmaf_rn(-dist, c2, g);
+  }
+  float wt = ex2_approx(arg);
+  wt = k ? wt : 0.0f;
+  bw = __fadd_rn(bw, wt);
+  bj = __fmaf_rn(wt, (float)(c.w & 0xffu), bj);
+}
+
+// Certification.  Notation: w_i the reference's FP64 weights of the survivors
+// (in order), W_ref / J_ref its sequential sums, rho_ref = fl(J_ref / W_ref).
+//  (1) Per survivor, |ln(w_hat_i / w_i)| <= lam (host part a.lam, see
+//      certified_lambda(), plus the pixel-position term below), from: two-float
+//      pixel position (dx error <= 2.01 e32 |dx| + 2.01 e32^2 |w|), f32 squares,
+//      rsqrt.approx (kRsqErr), f32 gate A2 and scale c2 (one rounding each),
+//      the FMA exponent, ex2.approx (kEx2Err), the reference's own FP64 chain
+//      (<= 16 e64 M) and glibc exp (<= 2 e64).
+//  (2) Batch sums of <= 4 non-negative f32 terms: bw <= 3 roundings, bj <= 4
+//      (FMA); f64 accumulation of the batch sums and the reference's sums of
+//      n <= V terms: <= (2.1 V + 2) e64 together.
+//  =>  W_ref in W_hat * exp(+-eW), J_ref in J_hat * exp(+-eJ),
+//      rho_ref in rho_hat * exp(+-(eW + eJ + 3 e64)).
+//  The reference's decision g(x) = clamp(floor(fl(x + 0.5))) is monotone in x,
+//  so if g agrees at both ends of rho's interval it equals g(rho_ref); the
+//  coverage test W_ref >= 1e-12 is decided the same way.  Otherwise (or on any
+//  NaN) the pixel goes to the exact path.  exp(x) <= 1 + 1.01 x for the x here
+//  (< 1e-3); the 1.01 also absorbs the f64 rounding of the bound arithmetic.
+__device__ __forceinline__ bool certify(const ResliceArgs& a, const Walk& w, float c2, double W,
+                                        double J, uint32_t visits, uint8_t& ov, uint8_t& oc) {
+  const double maxw = fmax(fabs(w.wx), fmax(fabs(w.wy), fabs(w.wz)));
+  const double lam = a.lam + kLn2 * (double)c2 * (2.5e-14 * maxw + 1e-15);
+  const double vt = (2.1 * (double)visits + 2.0) * kEps64;
+  const double eW = lam + 3.1 * kEps32 + vt;
+  const double eJ = lam + 4.1 * kEps32 + vt;
+  if (W * (1.0 - 1.01 * eW) >= kCoverageMinWeight) {
+    const double rho = J / W;
+    const double E = 1.01 * (eW + eJ + 3.0 * kEps64);
+    double glo = floor(rho * (1.0 - E) + 0.5), ghi = floor(rho * (1.0 + E) + 0.5);
+    glo = glo < 0.0 ? 0.0 : (glo > 255.0 ? 255.0 : glo);
+    ghi = ghi < 0.0 ? 0.0 : (ghi > 255.0 ? 255.0 : ghi);
+    if (!(glo == ghi)) return false;
+    ov = (uint8_t)glo;
+    oc = 1;
+    return true;
+  }
+  if (W * (1.0 + 1.01 * eW) < kCoverageMinWeight) {
+    ov = (uint8_t)a.unassigned;
+    oc = 0;
+    return true;
+  }
+  return false;
+}
+
+// Certified path: same mapping and walk as reslice_k, but branch-free f32
+// weights for every visited record (no warp rounds), 4 loads in flight.
+template <int kDistMode>
+__global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
+                                                      uint8_t* __restrict__ cov) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int pose, u, v;
+  bool active;
+  map_pixel(a, pose, u, v, active);
+  bool any_rejected;
+  const float* gate = stage_gate<float, kGateSmemF>(a, a.gate2 + (size_t)pose * a.n_orient,
+                                                    reinterpret_cast<float*>(smem_raw), any_rejected);
+  Walk w;
+  w.init(a, pose, u, v, active, true);
+  int jx = 0, jy = 0;
+  if (w.live) w.live = w.open_run_phased(a, jx, jy);
+  const float wh[3] = {__double2float_rn(w.wx), __double2float_rn(w.wy), __double2float_rn(w.wz)};
+  const float wl[3] = {__double2float_rn(w.wx - (double)wh[0]), __double2float_rn(w.wy - (double)wh[1]),
+                       __double2float_rn(w.wz - (double)wh[2])};
+  const float c2 = a.c2;
+  double W = 0.0, J = 0.0;
+  uint32_t visits = 0;
+  uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
+  while (w.live) {
+    const uint32_t n = min(4u, w.e - w.s);
+    const uint4* __restrict__ q = a.records + w.s;
+    r0 = __ldg(q);
+    if (n > 1) r1 = __ldg(q + 1);
+    if (n > 2) r2 = __ldg(q + 2);
+    if (n > 3) r3 = __ldg(q + 3);
+    w.s += n;
+    visits += n;
+    float bw = 0.0f, bj = 0.0f;
+    fast_term<kDistMode>(r0, true, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode>(r1, n > 1, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode>(r2, n > 2, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode>(r3, n > 3, w, gate, wh, wl, c2, bw, bj);
+    W += (double)bw;
+    J += (double)bj;
+    if (w.s == w.e) w.live = w.open_run_phased(a, jx, jy);
+  }
+  if (!active) return;
+  const size_t k = ((size_t)pose * a.H + v) * a.W + u;
+  uint8_t ov, oc;
+  if (certify(a, w, c2, W, J, visits, ov, oc)) {
+    out[k] = ov;
+    cov[k] = oc;
+  } else {
+    const unsigned slot = atomicAdd(a.amb_count, 1u);
+    if (slot < a.amb_cap) a.amb[slot] = k;
+  }
+}
+
+// Exact recomputation of the pixels the certified path could not decide (all
+// pixels of the launch if the list overflowed): one warp per pixel, so a
+// handful of undecided pixels costs one short walk, not a serial one.
+template <int kDistMode>
+__global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t* __restrict__ out,
+                                                       uint8_t* __restrict__ cov) {
+  const unsigned n = *a.amb_count;
+  const bool all = n > a.amb_cap;
+  const uint64_t total = all ? (uint64_t)a.P * a.H * a.W : (uint64_t)n;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.fallback_total)
+    atomicAdd(a.fallback_total, (unsigned long long)total);
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += warps) {
+    const uint64_t k = all ? i : a.amb[i];
+    const int u = (int)(k % (uint64_t)a.W);
+    const uint64_t t = k / (uint64_t)a.W;
+    const int v = (int)(t % (uint64_t)a.H);
+    const int pose = (int)(t / (uint64_t)a.H);
+    Walk w;
+    w.init(a, pose, u, v, true);
+    double wsum, iwsum;
+    exact_sums_warp<kDistMode>(w, a, a.gate + (size_t)pose * a.n_orient, wsum, iwsum);
+    if ((threadIdx.x & 31) == 0) write_exact(a, k, wsum, iwsum, out, cov);
   }
 }
 
@@ -299,9 +600,97 @@ __global__ void exp_k(const double* x, double* y, int64_t n) {
   if (i < n) y[i] = dare_exp(x[i]);
 }
 
+// ---- hardware approximation check ----------------------------------------
+// Max relative error of ex2.approx (which = 0) or rsqrt.approx (which = 1)
+// over the f32 bit patterns [lo, lo + count), against FP64 references; a NaN
+// or infinite error counts as 1.  Non-negative doubles order like their bits.
+__global__ void mufu_check_k(int which, uint32_t lo, uint64_t count, unsigned long long* maxerr) {
+  double m = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const float x = __uint_as_float(lo + (uint32_t)i);
+    double got, ref;
+    if (which == 0) {
+      got = (double)ex2_approx(x);
+      ref = exp2((double)x);
+    } else {
+      got = (double)rsqrt_approx(x);
+      ref = 1.0 / sqrt((double)x);
+    }
+    double err = fabs(got - ref) / ref;
+    if (!(err <= 1.0)) err = 1.0;
+    m = fmax(m, err);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxerr, (unsigned long long)__double_as_longlong(m));
+}
+
+static void fastmath_measure(cudaStream_t s, double* ex2_err, double* rsq_err) {
+  Scratch<unsigned long long> d(2, s);
+  DARE_CUDA(cudaMemsetAsync(d.ptr, 0, 2 * sizeof(unsigned long long), s));
+  const unsigned grid = (unsigned)sm_count() * 8;
+  auto bits = [](float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+  };
+  // ex2 on every f32 in [-kMaxLog2Arg, kMaxLog2Arg] (both signs, incl. subnormals / zeros)
+  const uint32_t top = bits((float)kMaxLog2Arg);
+  mufu_check_k<<<grid, 256, 0, s>>>(0, 0u, (uint64_t)top + 1, d.ptr);
+  mufu_check_k<<<grid, 256, 0, s>>>(0, 0x80000000u, (uint64_t)top + 1, d.ptr);
+  // rsqrt on every finite f32 >= 1e-30 (the clamp floor of d2)
+  const uint32_t lo = bits(1e-30f);
+  mufu_check_k<<<grid, 256, 0, s>>>(1, lo, (uint64_t)0x7f7fffffu - lo + 1, d.ptr + 1);
+  DARE_CUDA(cudaGetLastError());
+  unsigned long long h[2];
+  DARE_CUDA(cudaMemcpyAsync(h, d.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaStreamSynchronize(s));
+  memcpy(ex2_err, &h[0], 8);
+  memcpy(rsq_err, &h[1], 8);
+}
+
+// Per-device cache of the check (run on first certified launch).
+static bool fastmath_ok(cudaStream_t s) {
+  static std::mutex mu;
+  static int state[256] = {0};  // 0 unknown, 1 ok, -1 failed
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 256) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (state[dev] == 0) {
+    double e1 = 1.0, e2 = 1.0;
+    fastmath_measure(s, &e1, &e2);
+    state[dev] = (e1 <= kEx2Err && e2 <= kRsqErr) ? 1 : -1;
+  }
+  return state[dev] == 1;
+}
+
+// Host part of the per-survivor bound (see certify()): M bounds |A2| + |t2|
+// (log2 units) for every survivor -- gates admit d_n >= cos_n, d_i >= cos_i,
+// the cube bounds dist <= r sqrt(3).  Returns a negative value when the fast
+// path must not be used (weights could leave ex2's accurate range).
+static double certified_lambda(const dare_reslice_cfg& c) {
+  auto span = [](double cs) {
+    double d = 1.0 - cs;
+    if (!(d <= 2.0)) d = 2.0;  // also NaN
+    if (d < 0.0) d = 0.0;
+    return d + 1e-12;
+  };
+  const double M = (kLog2e * (fabs(c.k_normal) * span(c.cos_normal) + fabs(c.k_inplane) * span(c.cos_inplane) +
+                              fabs(c.k_dist) * 1.7320508075688774) * (1.0 + 1e-9)) + 1e-9;
+  if (!(M <= kMaxLog2Arg - 1.0)) return -1.0;
+  return kLn2 * (9.0 * kEps32 + kRsqErr + 16.0 * kEps64) * M + 1.01 * kEx2Err + 3.0 * kEps64;
+}
+
+template <class K>
+static void set_smem(K kernel) {
+  DARE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+}
+
 static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params, int32_t W,
                            int32_t H, const dare_reslice_cfg* cfg, uint8_t* d_pixels,
-                           uint8_t* d_cov, cudaStream_t s, int brute = 0, bool coherent = false) {
+                           uint8_t* d_cov, cudaStream_t s, int brute = 0, bool coherent = false,
+                           unsigned long long* d_fallback_total = nullptr) {
   DARE_REQUIRE(vol != nullptr && cfg != nullptr, "null argument");
   DARE_REQUIRE(W > 0 && H > 0, "reslice plane must have at least one pixel");
   DARE_REQUIRE(P >= 0 && P <= 65535, "n_poses must be in [0, 65535] per launch");
@@ -321,6 +710,8 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.kd = cfg->k_dist;
   a.inv_radius = 1.0 / cfg->radius;
   a.dist_mode = cfg->k_dist == 0.0 ? 2 : (exact_reciprocal(cfg->radius) ? 1 : 0);
+  a.c2 = (float)(cfg->k_dist * kLog2e / cfg->radius);
+  a.lam = certified_lambda(*cfg);
   a.unassigned = cfg->unassigned;
   a.W = W;
   a.H = H;
@@ -328,13 +719,20 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.tiles_x = (int)ceil_div(W, 16);
   a.brute = brute;
   a.n_samples = (uint32_t)vol->n_samples;
+  a.amb = nullptr;
+  a.amb_count = nullptr;
+  a.amb_cap = 0;
+  a.fallback_total = d_fallback_total;
+  const bool fast = !brute && cfg->exact == 0 && a.lam > 0.0 && std::isfinite(a.c2) && fastmath_ok(s);
   const int tiles_y = (int)ceil_div(H, 16);
   PhaseTimer pt(s, "reslice");
   Scratch<double> gate((size_t)P * a.n_orient, s);
+  Scratch<float> gate2((size_t)P * a.n_orient, s);
   a.gate = gate.ptr;
+  a.gate2 = gate2.ptr;
   if (vol->n_orient > 0) {
     gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient,
-                                                                 d_params, P, *cfg, gate.ptr);
+                                                                 d_params, P, *cfg, gate.ptr, gate2.ptr);
     DARE_CUDA(cudaGetLastError());
   }
   pt.mark("gate");
@@ -357,26 +755,56 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   pt.mark("order");
   const dim3 grid = a.pose_major ? dim3(ceil_div(W, 4) * ceil_div(H, 2), ceil_div(P, 32))
                                   : dim3(a.tiles_x * tiles_y, P);
-  static bool attr_done = false;  // benign race: idempotent attribute set
-  if (!attr_done) {
-    DARE_CUDA(cudaFuncSetAttribute(reslice_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    DARE_CUDA(cudaFuncSetAttribute(reslice_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    DARE_CUDA(cudaFuncSetAttribute(reslice_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    attr_done = true;
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    set_smem(reslice_k<0>);
+    set_smem(reslice_k<1>);
+    set_smem(reslice_k<2>);
+    set_smem(reslice_fast_k<0>);
+    set_smem(reslice_fast_k<1>);
+    set_smem(reslice_fast_k<2>);
+  });
+  if (!fast) {
+    if (a.dist_mode == 0)
+      reslice_k<0><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+    else if (a.dist_mode == 1)
+      reslice_k<1><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+    else
+      reslice_k<2><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+    pt.mark("reslice_k");
+    DARE_CUDA(cudaGetLastError());
+    return;
   }
-  if (a.dist_mode == 0)
-    reslice_k<0><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else if (a.dist_mode == 1)
-    reslice_k<1><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  // Ambiguity list: 1/16 of the launch's pixels (overflow -> exact recompute of all).
+  const uint64_t npix = (uint64_t)P * W * H;
+  a.amb_cap = (unsigned)std::min<uint64_t>(std::max<uint64_t>(npix / 16, 4096), 1u << 30);
+  Scratch<unsigned long long> amb(a.amb_cap, s);
+  Scratch<unsigned> amb_count(1, s);
+  a.amb = amb.ptr;
+  a.amb_count = amb_count.ptr;
+  DARE_CUDA(cudaMemsetAsync(amb_count.ptr, 0, sizeof(unsigned), s));
+  if (a.dist_mode == 2)
+    reslice_fast_k<2><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   else
-    reslice_k<2><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  pt.mark("reslice_k");
+    reslice_fast_k<0><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  pt.mark("reslice_fast_k");
+  DARE_CUDA(cudaGetLastError());
+  const unsigned fb_grid = (unsigned)sm_count() * 2;
+  if (a.dist_mode == 0)
+    reslice_fallback_k<0><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
+  else if (a.dist_mode == 1)
+    reslice_fallback_k<1><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
+  else
+    reslice_fallback_k<2><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
+  pt.mark("fallback");
   DARE_CUDA(cudaGetLastError());
 }
 
 }  // namespace dare
 
 using namespace dare;
+
+static thread_local int64_t tl_last_fallback = 0;
 
 extern "C" int dare_reslice_device(dare_volume_t vol, int32_t n_poses, const double* d_params,
                                    int32_t width, int32_t height, const dare_reslice_cfg* cfg,
@@ -415,11 +843,14 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
                          uint8_t* coverage, int brute) {
   DARE_REQUIRE(n_poses >= 0, "negative pose count");
   DARE_REQUIRE(width > 0 && height > 0, "reslice plane must have at least one pixel");
+  tl_last_fallback = 0;
   if (n_poses == 0) return;
   cudaStream_t s = thread_stream();
   const size_t npix = (size_t)n_poses * width * height;
   Scratch<double> d_params((size_t)n_poses * 14, s);
   Scratch<uint8_t> d_out(2 * npix, s);
+  Scratch<unsigned long long> d_fb(1, s);
+  DARE_CUDA(cudaMemsetAsync(d_fb.ptr, 0, sizeof(unsigned long long), s));
   DARE_CUDA(cudaMemcpyAsync(d_params.ptr, params, sizeof(double) * 14 * n_poses,
                             cudaMemcpyHostToDevice, s));
   for (int32_t p0 = 0; p0 < n_poses; p0 += 65535) {
@@ -427,11 +858,14 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
     size_t off = (size_t)p0 * width * height;
     launch_reslice(vol, np, d_params.ptr + (size_t)p0 * 14, width, height, cfg, d_out.ptr + off,
                    d_out.ptr + npix + off, s, brute,
-                   poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel));
+                   poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel), d_fb.ptr);
   }
+  unsigned long long fb = 0;
   DARE_CUDA(cudaMemcpyAsync(pixels, d_out.ptr, npix, cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaMemcpyAsync(coverage, d_out.ptr + npix, npix, cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaMemcpyAsync(&fb, d_fb.ptr, sizeof(fb), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
+  tl_last_fallback = (int64_t)fb;
 }
 
 extern "C" int dare_reslice(dare_volume_t vol, int32_t n_poses, const double* params,
@@ -444,6 +878,23 @@ extern "C" int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const
                                        int32_t width, int32_t height, const dare_reslice_cfg* cfg,
                                        uint8_t* pixels, uint8_t* coverage) {
   return guard([&] { reslice_host(vol, n_poses, params, width, height, cfg, pixels, coverage, 1); });
+}
+
+extern "C" int dare_reslice_last_fallback(int64_t* n_pixels) {
+  return guard([&] {
+    DARE_REQUIRE(n_pixels != nullptr, "null argument");
+    *n_pixels = tl_last_fallback;
+  });
+}
+
+extern "C" int dare_fastmath_check(double* ex2_max_rel_err, double* rsqrt_max_rel_err, int32_t* ok) {
+  return guard([&] {
+    double e1 = 1.0, e2 = 1.0;
+    fastmath_measure(thread_stream(), &e1, &e2);
+    if (ex2_max_rel_err) *ex2_max_rel_err = e1;
+    if (rsqrt_max_rel_err) *rsqrt_max_rel_err = e2;
+    if (ok) *ok = (e1 <= kEx2Err && e2 <= kRsqErr) ? 1 : 0;
+  });
 }
 
 extern "C" int dare_poses_coherent(const double* params, int32_t n_poses, int32_t width,

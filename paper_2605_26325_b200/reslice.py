@@ -118,11 +118,14 @@ def plane_params(plane) -> tuple[float, ...]:
             float(plane.pixel_pitch[0]), float(plane.pixel_pitch[1]))
 
 
-def kernel_cfg(cfg, schedule: int = 0) -> _lib.ResliceCfg:
-    """Kernel scalars; schedule 0 = auto, 1 = pixel-major, 2 = pose-major."""
+def kernel_cfg(cfg, schedule: int = 0, exact: bool = False) -> _lib.ResliceCfg:
+    """Kernel scalars; schedule 0 = auto, 1 = pixel-major, 2 = pose-major;
+    exact=True forces FP64 reference arithmetic for every pixel (the default
+    certified path gives the same pixels, see csrc/reslice.cu)."""
     return _lib.ResliceCfg(float(cfg.interp_radius), float(cfg.cos_normal_threshold),
                            float(cfg.cos_inplane_threshold), float(cfg.k_normal),
-                           float(cfg.k_inplane), float(cfg.k_dist), int(cfg.unassigned_value), int(schedule))
+                           float(cfg.k_inplane), float(cfg.k_dist), int(cfg.unassigned_value), int(schedule),
+                           1 if exact else 0, 0)
 
 
 def _run(fn: str, volume, planes, cfg):

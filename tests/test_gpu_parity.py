@@ -304,3 +304,95 @@ def test_darevol_from_device_volume_identical(golden, tmp_path):
     path = tmp_path / "v.darevol"
     db.save_volume(v, path)
     assert hashlib.sha256(path.read_bytes()).hexdigest() == str(golden["rec_tilt.darevol_sha256"])
+
+
+# ---------------------------------------------------------------- certified path
+
+def _fallback_pixels():
+    import ctypes
+
+    n = ctypes.c_int64()
+    _lib.call("dare_reslice_last_fallback", ctypes.byref(n))
+    return n.value
+
+
+def _reslice_raw(vol, planes, cfg, exact, schedule=0):
+    import ctypes
+
+    from paper_2605_26325_b200.reslice import kernel_cfg, plane_params
+
+    w, h = planes[0].width, planes[0].height
+    params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
+    px = np.empty((len(planes), h, w), np.uint8)
+    cv = np.empty((len(planes), h, w), np.uint8)
+    kc = kernel_cfg(cfg, schedule, exact)
+    _lib.call("dare_reslice", vol.device_handle().raw, len(planes), _lib.ptr(params, ctypes.c_double), w, h,
+              ctypes.byref(kc), _lib.ptr(px, ctypes.c_uint8), _lib.ptr(cv, ctypes.c_uint8))
+    return px, cv, _fallback_pixels()
+
+
+def test_fastmath_constants_hold_exhaustively():
+    """Every f32 input of ex2.approx / rsqrt.approx in the ranges the certified
+    bound uses is within the assumed 2^-21 relative error on this device."""
+    import ctypes
+
+    e1, e2, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+    _lib.call("dare_fastmath_check", ctypes.byref(e1), ctypes.byref(e2), ctypes.byref(ok))
+    print(f"ex2.approx max rel err {e1.value:.3e}, rsqrt.approx max rel err {e2.value:.3e}")
+    assert ok.value == 1
+    assert 0 < e1.value <= 2.0 ** -21 and 0 < e2.value <= 2.0 ** -21
+
+
+def test_certified_path_equals_exact_path(rng):
+    """Default (certified f32 + exact fallback) and exact=1 (FP64 everywhere)
+    give identical pixels over random volumes, planes and configs, both
+    schedules."""
+    for case in range(30):
+        vol = _random_volume(rng, int(rng.integers(2000, 40_001)), 10.0, float(rng.choice([0.25, 0.5])))
+        planes = []
+        for _ in range(int(rng.integers(1, 40))):
+            q = rng.normal(size=4)
+            q /= np.linalg.norm(q)
+            planes.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(1, 9, 3)), 21, 17,
+                                       (float(rng.uniform(0.1, 0.4)),) * 2))
+        cfg = ResliceConfig(interp_radius=float(rng.uniform(0.15, 1.0)),
+                            normal_threshold_deg=float(rng.uniform(5, 89)),
+                            inplane_threshold_deg=float(rng.uniform(5, 89)), k_normal=float(rng.uniform(0, 20)),
+                            k_inplane=float(rng.uniform(0, 10)), k_dist=float(rng.choice([0.0, 0.5, 2.0, 4.0])),
+                            unassigned_value=int(rng.integers(0, 256)))
+        ex = _reslice_raw(vol, planes, cfg, True)
+        assert ex[2] == 0
+        for sched in (1, 2):
+            fa = _reslice_raw(vol, planes, cfg, False, sched)
+            np.testing.assert_array_equal(fa[0], ex[0], err_msg=f"case {case} sched {sched}")
+            np.testing.assert_array_equal(fa[1], ex[1], err_msg=f"case {case} sched {sched}")
+
+
+def _lattice_volume(rng, n=24, spacing=0.125):
+    """Samples on an exact f32 lattice, one orientation, random intensities:
+    equal weights (k_dist = 0) or symmetric distances make half-integer
+    weighted means common -- the cases the certified bound cannot decide."""
+    g = np.arange(n, dtype=np.float64) * spacing + spacing / 2
+    pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    q = np.tile([1.0, 0.0, 0.0, 0.0], (len(pos), 1))
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (n * spacing,) * 3), 0.25)
+    b.insert_batch(pos, q, rng.integers(0, 256, len(pos)))
+    return b.seal()
+
+
+@pytest.mark.parametrize("k_dist", [0.0, 2.0])
+def test_half_integer_ties_take_the_exact_fallback(rng, k_dist):
+    vol = _lattice_volume(rng)
+    planes = [ReslicePlane(Pose(Quaternion.identity(), (0.0, 0.0, 0.0625 + 0.125 * k)), 24, 24, (0.125, 0.125))
+              for k in range(8)]
+    cfg = ResliceConfig(interp_radius=0.125, k_dist=k_dist)
+    fa = _reslice_raw(vol, planes, cfg, False)
+    ex = _reslice_raw(vol, planes, cfg, True)
+    assert fa[2] > 0, "lattice ties should reach the exact fallback"
+    np.testing.assert_array_equal(fa[0], ex[0])
+    np.testing.assert_array_equal(fa[1], ex[1])
+    for k, p in enumerate(planes[:3]):
+        ref = oracle.reslice(vol, oracle.plane_params(p), oracle.cfg_array(cfg), p.width, p.height,
+                             cfg.unassigned_value)
+        np.testing.assert_array_equal(fa[0][k], ref[0], err_msg=f"plane {k}")
+        np.testing.assert_array_equal(fa[1][k].astype(bool), ref[1], err_msg=f"plane {k}")
