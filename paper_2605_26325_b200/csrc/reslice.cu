@@ -235,43 +235,12 @@ struct Walk {
     return false;
   }
 
-  // Certified path: the sums are order-independent (the bound does not depend
-  // on the order), so columns are visited in phases (cx mod 3, cy mod 3):
-  // within a phase, the 3x3 neighbouring pixels that share a column read it
-  // together (same addresses in the same warp instruction) instead of a third
-  // of the walk apart, which is what kept the column out of L1/L2 between its
-  // readers.  jx/jy are the phase; every column of the range is visited once.
-  __device__ __forceinline__ bool open_run_phased(const ResliceArgs& a, int& jx, int& jy) {
-    while (jx < 3) {
-      while (cx <= hix) {
-        const int64_t base0 = cx * a.dims[1];
-        while (cy <= hiy) {
-          const int64_t base = (base0 + cy) * a.dims[2];
-          s = __ldg(a.offsets + base + loz);
-          e = __ldg(a.offsets + base + hiz + 1);
-          cy += 3;
-          if (s < e) return true;
-        }
-        cx += 3;
-        cy = loy + (jy - loy % 3 + 3) % 3;
-      }
-      if (++jy == 3) {
-        jy = 0;
-        ++jx;
-      }
-      cx = lox + (jx - lox % 3 + 3) % 3;
-      cy = loy + (jy - loy % 3 + 3) % 3;
-    }
-    return false;
-  }
-
   __device__ __forceinline__ bool in_cube(const uint4& c) const {
     const float x = __uint_as_float(c.x), y = __uint_as_float(c.y), z = __uint_as_float(c.z);
     return x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi;
   }
 
-  __device__ __forceinline__ void init(const ResliceArgs& a, int pose, int u, int v, bool active,
-                                       bool phased = false) {
+  __device__ __forceinline__ void init(const ResliceArgs& a, int pose, int u, int v, bool active) {
     const double* pp = a.params + (size_t)pose * 14;
     const double du = (double)u * pp[12], dv = (double)v * pp[13];
     wx = (pp[0] + du * pp[3]) + dv * pp[4];
@@ -287,15 +256,9 @@ struct Walk {
     zlo = keep_lo(wz, r), zhi = keep_hi(wz, r);
     s = e = 0;
     const bool nonempty = a.brute ? true : (lox <= hix && loy <= hiy && loz <= hiz);
-    if (phased) {  // phase (0, 0): first column with cx = cy = 0 (mod 3); caller opens
-      cx = lox + (3 - lox % 3) % 3;
-      cy = loy + (3 - loy % 3) % 3;
-      live = active && nonempty;
-    } else {
-      cx = lox;
-      cy = loy;
-      live = active && nonempty && open_run(a);
-    }
+    cx = lox;
+    cy = loy;
+    live = active && nonempty && open_run(a);
   }
 };
 
@@ -426,13 +389,56 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
   if (active) write_exact(a, ((size_t)pose * a.H + v) * a.W + u, wsum, iwsum, out, cov);
 }
 
+// Certified-path walker: the survivor test of Walk with 32-bit cell indices
+// and no FP64 state in the loop (registers), columns visited in phases.
+struct FastWalk {
+  float xlo, xhi, ylo, yhi, zlo, zhi;
+  int lox, hix, loy, hiy, loz, hiz, cx, cy, jx, jy;
+  uint32_t s, e;
+
+  // Columns in phases (cx mod 3, cy mod 3): within a phase, the 3x3
+  // neighbouring pixels that share a column read it together (same addresses
+  // in the same warp instruction) instead of a third of the walk apart.  The
+  // certified sums are order-independent; every column is visited once.
+  __device__ __forceinline__ bool open(const ResliceArgs& a, uint32_t& visits) {
+    while (jx < 3) {
+      while (cx <= hix) {
+        while (cy <= hiy) {
+          const int64_t base = ((int64_t)cx * a.dims[1] + cy) * a.dims[2];
+          s = __ldg(a.offsets + base + loz);
+          e = __ldg(a.offsets + base + hiz + 1);
+          cy += 3;
+          if (s < e) {
+            visits += e - s;
+            return true;
+          }
+        }
+        cx += 3;
+        cy = loy + (jy - loy % 3 + 3) % 3;
+      }
+      if (++jy == 3) {
+        jy = 0;
+        ++jx;
+      }
+      cx = lox + (jx - lox % 3 + 3) % 3;
+      cy = loy + (jy - loy % 3 + 3) % 3;
+    }
+    return false;
+  }
+
+  __device__ __forceinline__ bool in_cube(const uint4& c) const {
+    const float x = __uint_as_float(c.x), y = __uint_as_float(c.y), z = __uint_as_float(c.z);
+    return x >= xlo && x <= xhi && y >= ylo && y <= yhi && z >= zlo && z <= zhi;
+  }
+};
+
 // One visited record on the certified path: exact survivor test, f32 weight
 // 2^(A2 - dist * c2) (0 for non-survivors), accumulated into the batch sums.
-template <int kDistMode>
-__device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Walk& w,
+template <int kDistMode, bool kSmemGate>
+__device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
                                           const float* gate, const float (&wh)[3],
                                           const float (&wl)[3], float c2, float& bw, float& bj) {
-  const float g = gate[c.w >> 8];
+  const float g = kSmemGate ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8));
   const bool k = valid && w.in_cube(c) && g != CUDART_INF_F;
   float arg = g;
   if (kDistMode != 2) {
@@ -443,10 +449,11 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Walk
     const float dist = __fmul_rn(d2, rsqrt_approx(fmaxf(d2, 1e-30f)));
     arg = __fmaf_rn(-dist, c2, g);
   }
-  float wt = ex2_approx(arg);
-  wt = k ? wt : 0.0f;
+  const float wt = k ? ex2_approx(arg) : 0.0f;
+  // intensity as f32 without I2F: bits 2^23 + I, minus 2^23 (exact)
+  const float inten = __fsub_rn(__uint_as_float(__byte_perm(c.w, 0x4B00u, 0x5440u)), 8388608.0f);
   bw = __fadd_rn(bw, wt);
-  bj = __fmaf_rn(wt, (float)(c.w & 0xffu), bj);
+  bj = __fmaf_rn(wt, inten, bj);
 }
 
 // Certification.  Notation: w_i the reference's FP64 weights of the survivors
@@ -467,9 +474,8 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Walk
 //  coverage test W_ref >= 1e-12 is decided the same way.  Otherwise (or on any
 //  NaN) the pixel goes to the exact path.  exp(x) <= 1 + 1.01 x for the x here
 //  (< 1e-3); the 1.01 also absorbs the f64 rounding of the bound arithmetic.
-__device__ __forceinline__ bool certify(const ResliceArgs& a, const Walk& w, float c2, double W,
+__device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float c2, double W,
                                         double J, uint32_t visits, uint8_t& ov, uint8_t& oc) {
-  const double maxw = fmax(fabs(w.wx), fmax(fabs(w.wy), fabs(w.wz)));
   const double lam = a.lam + kLn2 * (double)c2 * (2.5e-14 * maxw + 1e-15);
   const double vt = (2.1 * (double)visits + 2.0) * kEps64;
   const double eW = lam + 3.1 * kEps32 + vt;
@@ -493,51 +499,81 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, const Walk& w, flo
   return false;
 }
 
-// Certified path: same mapping and walk as reslice_k, but branch-free f32
-// weights for every visited record (no warp rounds), 4 loads in flight.
-template <int kDistMode>
+// Certified path: same mapping as reslice_k; branch-free f32 weights for
+// every visited record (no warp rounds), 4 loads in flight, phased walk.
+template <int kDistMode, bool kSmemGate>
 __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                       uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
   map_pixel(a, pose, u, v, active);
-  bool any_rejected;
-  const float* gate = stage_gate<float, kGateSmemF>(a, a.gate2 + (size_t)pose * a.n_orient,
-                                                    reinterpret_cast<float*>(smem_raw), any_rejected);
-  Walk w;
-  w.init(a, pose, u, v, active, true);
-  int jx = 0, jy = 0;
-  if (w.live) w.live = w.open_run_phased(a, jx, jy);
-  const float wh[3] = {__double2float_rn(w.wx), __double2float_rn(w.wy), __double2float_rn(w.wz)};
-  const float wl[3] = {__double2float_rn(w.wx - (double)wh[0]), __double2float_rn(w.wy - (double)wh[1]),
-                       __double2float_rn(w.wz - (double)wh[2])};
+  const float* gate = a.gate2 + (size_t)pose * a.n_orient;
+  if (kSmemGate) {  // pixel-major launch: one pose per block
+    float* sg = reinterpret_cast<float*>(smem_raw);
+    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) sg[i] = gate[i];
+    __syncthreads();
+    gate = sg;
+  }
+  FastWalk w;
+  float wh[3], wl[3];
+  double maxw;
+  bool live;
+  {
+    const double* pp = a.params + (size_t)pose * 14;
+    const double du = (double)u * pp[12], dv = (double)v * pp[13];
+    const double wx = (pp[0] + du * pp[3]) + dv * pp[4];
+    const double wy = (pp[1] + du * pp[6]) + dv * pp[7];
+    const double wz = (pp[2] + du * pp[9]) + dv * pp[10];
+    const double r = a.radius;
+    const double inv_v = 1.0 / a.voxel;
+    int64_t lo, hi;
+    cell_range(wx, r, a.origin[0], inv_v, a.dims[0], lo, hi);
+    w.lox = (int)lo, w.hix = (int)hi;
+    cell_range(wy, r, a.origin[1], inv_v, a.dims[1], lo, hi);
+    w.loy = (int)lo, w.hiy = (int)hi;
+    cell_range(wz, r, a.origin[2], inv_v, a.dims[2], lo, hi);
+    w.loz = (int)lo, w.hiz = (int)hi;
+    w.xlo = keep_lo(wx, r), w.xhi = keep_hi(wx, r);
+    w.ylo = keep_lo(wy, r), w.yhi = keep_hi(wy, r);
+    w.zlo = keep_lo(wz, r), w.zhi = keep_hi(wz, r);
+    wh[0] = __double2float_rn(wx), wh[1] = __double2float_rn(wy), wh[2] = __double2float_rn(wz);
+    wl[0] = __double2float_rn(wx - (double)wh[0]);
+    wl[1] = __double2float_rn(wy - (double)wh[1]);
+    wl[2] = __double2float_rn(wz - (double)wh[2]);
+    maxw = fmax(fabs(wx), fmax(fabs(wy), fabs(wz)));
+    w.jx = w.jy = 0;
+    w.cx = w.lox + (3 - w.lox % 3) % 3;
+    w.cy = w.loy + (3 - w.loy % 3) % 3;
+    w.s = w.e = 0;
+    live = active && w.lox <= w.hix && w.loy <= w.hiy && w.loz <= w.hiz;
+  }
+  uint32_t visits = 0;
+  if (live) live = w.open(a, visits);
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
-  uint32_t visits = 0;
-  uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
-  while (w.live) {
+  while (live) {
     const uint32_t n = min(4u, w.e - w.s);
     const uint4* __restrict__ q = a.records + w.s;
-    r0 = __ldg(q);
-    if (n > 1) r1 = __ldg(q + 1);
-    if (n > 2) r2 = __ldg(q + 2);
-    if (n > 3) r3 = __ldg(q + 3);
+    // unconditional loads (clamped to the run): no branches around them
+    const uint4 r0 = __ldg(q);
+    const uint4 r1 = __ldg(q + min(1u, n - 1));
+    const uint4 r2 = __ldg(q + min(2u, n - 1));
+    const uint4 r3 = __ldg(q + min(3u, n - 1));
     w.s += n;
-    visits += n;
     float bw = 0.0f, bj = 0.0f;
-    fast_term<kDistMode>(r0, true, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode>(r1, n > 1, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode>(r2, n > 2, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode>(r3, n > 3, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode, kSmemGate>(r0, true, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode, kSmemGate>(r1, n > 1, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode, kSmemGate>(r2, n > 2, w, gate, wh, wl, c2, bw, bj);
+    fast_term<kDistMode, kSmemGate>(r3, n > 3, w, gate, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
-    if (w.s == w.e) w.live = w.open_run_phased(a, jx, jy);
+    if (w.s == w.e) live = w.open(a, visits);
   }
   if (!active) return;
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
   uint8_t ov, oc;
-  if (certify(a, w, c2, W, J, visits, ov, oc)) {
+  if (certify(a, maxw, c2, W, J, visits, ov, oc)) {
     out[k] = ov;
     cov[k] = oc;
   } else {
@@ -760,9 +796,10 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_k<0>);
     set_smem(reslice_k<1>);
     set_smem(reslice_k<2>);
-    set_smem(reslice_fast_k<0>);
-    set_smem(reslice_fast_k<1>);
-    set_smem(reslice_fast_k<2>);
+    set_smem(reslice_fast_k<0, true>);
+    set_smem(reslice_fast_k<0, false>);
+    set_smem(reslice_fast_k<2, true>);
+    set_smem(reslice_fast_k<2, false>);
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -783,10 +820,11 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.amb = amb.ptr;
   a.amb_count = amb_count.ptr;
   DARE_CUDA(cudaMemsetAsync(amb_count.ptr, 0, sizeof(unsigned), s));
+  const bool smem_gate = !a.pose_major && a.n_orient <= kGateSmemF;
   if (a.dist_mode == 2)
-    reslice_fast_k<2><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+    (smem_gate ? reslice_fast_k<2, true> : reslice_fast_k<2, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   else
-    reslice_fast_k<0><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+    (smem_gate ? reslice_fast_k<0, true> : reslice_fast_k<0, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");
   DARE_CUDA(cudaGetLastError());
   const unsigned fb_grid = (unsigned)sm_count() * 2;
