@@ -12,7 +12,7 @@ content).  A step = one batch of B=64 reslice poses through the device path.
              per step H2D of 64 x 14 f64 pose params and D2H of pixels+coverage
   latency    p50/p95 of single-pose reslice() through the public API
   recon      reconstruct_volume input Mpix/s (frames in HBM, and e2e from pinned host)
-  roofline   dominant kernel (reslice_k) algorithmic bytes (SURVEY §8d
+  roofline   dominant kernel (reslice_fast_k) algorithmic bytes (SURVEY §8d
              reference-layout formula) / measured step time vs MEASURED_PEAKS hbm_gbs
   cpu_baseline  CPU oracle (oracle/, C + OpenMP) on a bounded sample (slab oracle)
 
@@ -279,9 +279,27 @@ def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
     call (frames in HBM); algorithmic bytes per SURVEY §8d."""
     from types import SimpleNamespace
 
+    from paper_2605_26325_b200 import parallel
+    from paper_2605_26325_b200.sweep import plan_frames
+
     n_in = wl.n_frames * wl.size * wl.size
     ms_c, sv = _best_ms(lambda: db.compound(dev_sweep, voxel_size=wl.voxel, margin=0.0))
     ncells = int(np.prod(sv.dims))
+    # device time of the accumulate kernel (+ zeroing the u64 sums/counts), CUDA events
+    plan = plan_frames(dev_sweep)
+    st = torch.cuda.Stream()
+    dev_c = []
+    with torch.cuda.stream(st):
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            acc = parallel.CudaOps.compound_partial(dev_sweep, plan, 0, plan.n_frames, sv.origin, sv.voxel_size,
+                                                    sv.dims, stream=st.cuda_stream)
+            e1.record(st)
+            st.synchronize()
+            dev_c.append(e0.elapsed_time(e1))
+            del acc
+    dev_ms_c = min(dev_c[1:])
     sparse = SimpleNamespace(images=frames_d[::8].contiguous(), image_timestamps=dev_sweep.image_timestamps[::8],
                              pose_timestamps=dev_sweep.pose_timestamps[::8], poses=dev_sweep.poses[::8],
                              pixel_pitch=dev_sweep.pixel_pitch, calibration=dev_sweep.calibration, mask=None)
@@ -298,7 +316,10 @@ def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
     gbs = lambda b, ms: b / (ms / 1000.0) / 1e9  # noqa: E731
     return {
         "compound": {"ms": ms_c, "input_Mpix_per_s": n_in / 1e6 / (ms_c / 1000.0),
-                     "algorithmic_GBps": gbs(comp_bytes, ms_c), "frac": gbs(comp_bytes, ms_c) / peak},
+                     "device_ms": dev_ms_c, "device_input_Mpix_per_s": n_in / 1e6 / (dev_ms_c / 1000.0),
+                     "algorithmic_GBps": gbs(comp_bytes, dev_ms_c), "frac": gbs(comp_bytes, dev_ms_c) / peak,
+                     "note": "ms = wall time of compound() (host plan + C-ABI call); device_ms = CUDA events "
+                             "around dare_compound_accumulate (zeroing + compound_k); frac uses device_ms"},
         "fill_holes": {"ms": ms_f, "passes_run": passes, "cells": nc_sparse,
                        "algorithmic_GBps": gbs(fill_bytes, ms_f) if passes else None,
                        "sweep": f"every 8th frame ({len(sparse.poses)} frames)"},
@@ -540,7 +561,8 @@ def run_b200(args):
     if args.exact:
         main_kernel = f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>"
     else:
-        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}>"
+        smem_gate = schedule == 1 and int(info.n_orientations) <= 1024
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {1 if smem_gate else 0}>"
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
     # [fallback kernel on the certified path]

@@ -141,6 +141,25 @@ __device__ __forceinline__ double voxel_coord(const VoxelMap& m, int a, float p3
   return m.exact_inv ? d * m.inv_voxel : d / m.voxel;
 }
 
+// Same map with the pixel's U = u * px and V = v * py precomputed (the
+// reference's arange(W) * px and arange(H) * py, reconstruct.py:156-158) and
+// the voxel division specialised at compile time (kInv: exact reciprocal).
+template <bool kInv>
+__device__ __forceinline__ int64_t frame_cell(const double* fa, double U, double V,
+                                              const VoxelMap& m) {
+  bool ok = true;
+  int idx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double P = (U * fa[a] + V * fa[3 + a]) + fa[6 + a];
+    const double d = (double)__double2float_rn(P) - m.origin[a];
+    const double f = floor(kInv ? d * m.inv_voxel : d / m.voxel);
+    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
+    idx[a] = ok ? (int)f : 0;
+  }
+  return ok ? ((int64_t)idx[0] * m.dims[1] + idx[1]) * m.dims[2] + idx[2] : -1;
+}
+
 // Pixel (u, v) of a frame with axes fa = {c0[3], c1[3], t[3]} ->
 // f32 world position (reconstruct.py:156-162) and linear cell (or -1 if out
 // of bounds; volume.py:229-230).

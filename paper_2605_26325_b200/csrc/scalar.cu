@@ -32,46 +32,71 @@ struct ScalarFrameView {
   double px, py;
 };
 
-// Same brick decomposition as the reconstruction scatter (csrc/reconstruct.cu):
-// a block keeps a 16(u) x 4(v) pixel tile and strides over groups of 4 frames,
-// each warp covers 8 x 2 x 2 (u, v, frame), so that pixels landing in one cell
-// (image neighbours and consecutive frames) share one pair of atomics.  Integer
-// sums make the result independent of the order (baseline.py:67).
-constexpr int kCBrickU = 16, kCBrickV = 4, kCBrickF = 4;
+// Thread = one pixel (u, v) over a chunk of kCFrames consecutive frames; warp
+// = an 8(u) x 4(v) patch, block = 16 x 16 pixels.  Each thread keeps a running
+// (cell, sum, count) and only flushes when its pixel moves to another cell --
+// consecutive frames of a sweep land in the same cell for several frames --
+// and a flush is warp-aggregated over lanes flushing the same cell (image
+// neighbours).  Integer sums make the result independent of the order
+// (baseline.py:67), so the atomics are exact.
+constexpr int kCFrames = 64;
 
+// Warp-converged flush: lanes with need=false get a unique non-cell key, so
+// MATCH / REDUX run once on the full warp (no divergent collective loops).
+__device__ __forceinline__ void compound_flush(bool need, int64_t lin, unsigned sum, unsigned cnt,
+                                               unsigned long long* sums, unsigned long long* counts) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned long long key = need ? (unsigned long long)lin : (0x8000000000000000ull | lane);
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const unsigned total = __reduce_add_sync(peers, sum);
+  const unsigned n = __reduce_add_sync(peers, cnt);
+  if (need && lane == (unsigned)(__ffs(peers) - 1)) {
+    atomicAdd(&sums[lin], (unsigned long long)total);
+    atomicAdd(&counts[lin], (unsigned long long)n);
+  }
+}
+
+template <bool kInv>
 __global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m,
                                                   unsigned long long* sums,
                                                   unsigned long long* counts) {
+  __shared__ double s_axes[kCFrames * 9];
+  __shared__ long long s_img[kCFrames];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t W = (uint32_t)fv.W, H = (uint32_t)fv.H;
-  const uint32_t tiles_u = (W + kCBrickU - 1) / kCBrickU;
-  const uint32_t u = (blockIdx.x % tiles_u) * kCBrickU + (warp & 1) * 8 + (lane & 7);
-  const uint32_t v = (blockIdx.x / tiles_u) * kCBrickV + ((warp >> 1) & 1) * 2 + ((lane >> 3) & 1);
-  const uint32_t fl = (warp >> 2) * 2 + (lane >> 4);
+  const uint32_t tiles_u = (W + 15) / 16;
+  const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
   const uint32_t p = v * W + u;
   const bool in_frame = u < W && v < H && (!fv.mask || fv.mask[p] != 0);
-  const size_t hw = (size_t)H * W;
-  for (int64_t f0 = (int64_t)blockIdx.y * kCBrickF; f0 < fv.n_frames; f0 += (int64_t)gridDim.y * kCBrickF) {
-    const int64_t f = f0 + fl;
-    const bool valid = in_frame && f < fv.n_frames;
+  const long long hw = (long long)H * W;
+  const int64_t f0 = (int64_t)blockIdx.y * kCFrames;
+  const int nf = (int)min((int64_t)kCFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[f0 * 9 + i];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (long long)fv.image[f0 + i] * hw;
+  __syncthreads();
+  const double U = (double)u * fv.px, V = (double)v * fv.py;
+  int64_t cur = -1;
+  unsigned sum = 0, cnt = 0;
+  for (int j = 0; j < nf; ++j) {  // block-uniform trip count
     int64_t lin = -1;
     unsigned inten = 0;
-    if (valid) {
-      float p32[3];
-      lin = pixel_cell(fv.axes + f * 9, (int)u, (int)v, fv.px, fv.py, m, p32);
-      inten = fv.frames[(size_t)fv.image[f] * hw + p];
+    if (in_frame) {
+      lin = frame_cell<kInv>(s_axes + j * 9, U, V, m);
+      inten = fv.frames[s_img[j] + p];
     }
-    const bool kept = lin >= 0;
-    const unsigned active = __ballot_sync(0xffffffffu, kept);
-    if (kept) {
-      const unsigned peers = __match_any_sync(active, (unsigned long long)lin);
-      const unsigned total = __reduce_add_sync(peers, inten);
-      if (lane == (unsigned)(__ffs(peers) - 1)) {
-        atomicAdd(&sums[lin], (unsigned long long)total);
-        atomicAdd(&counts[lin], (unsigned long long)__popc(peers));
-      }
+    const bool change = lin != cur;
+    const bool need = change && cur >= 0;
+    if (__any_sync(0xffffffffu, need)) compound_flush(need, cur, sum, cnt, sums, counts);
+    if (change) {
+      cur = lin;
+      sum = 0;
+      cnt = 0;
     }
+    sum += inten;
+    cnt += 1;
   }
+  if (__any_sync(0xffffffffu, cur >= 0)) compound_flush(cur >= 0, cur, sum, cnt, sums, counts);
 }
 
 __global__ void compound_finalize_k(int64_t n, const unsigned long long* __restrict__ sums,
@@ -309,10 +334,12 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
     const int64_t hw = (int64_t)height * width;
     if (n_frames > 0) {
       (void)hw;
-      dim3 grid(ceil_div(width, kCBrickU) * ceil_div(height, kCBrickV),
-                (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n_frames, kCBrickF), 1), 8));
-      compound_k<<<grid, 256, 0, s>>>(fv, m, (unsigned long long*)d_sums,
-                                      (unsigned long long*)d_counts);
+      PhaseTimer pt(s, "compound_accumulate");
+      DARE_LIMIT(ceil_div(n_frames, kCFrames) <= 65535, "too many frames for one compound launch");
+      dim3 grid(ceil_div(width, 16) * ceil_div(height, 16), ceil_div(n_frames, kCFrames));
+      (m.exact_inv ? compound_k<true> : compound_k<false>)<<<grid, 256, 0, s>>>(
+          fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
+      pt.mark("compound_k");
       DARE_CUDA(cudaGetLastError());
     }
     if (!frames_on_device || !stream) DARE_CUDA(cudaStreamSynchronize(s));
@@ -348,16 +375,20 @@ extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t he
     DARE_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
     cudaStream_t s = thread_stream();
     const int64_t ncells = dims[0] * dims[1] * dims[2];
+    PhaseTimer pt(s, "compound");
     Scratch<unsigned long long> acc(2 * ncells, s);
     DARE_CUDA(cudaMemsetAsync(acc.ptr, 0, sizeof(unsigned long long) * 2 * ncells, s));
+    pt.mark("alloc+memset");
     int rc = dare_compound_accumulate(frames, n_images, height, width, frames_on_device,
                                       frame_image, n_frames, frame_axes, pitch_x, pitch_y, mask,
                                       origin, voxel_size, dims, (uint64_t*)acc.ptr,
                                       (uint64_t*)(acc.ptr + ncells), (void*)s);
     if (rc != DARE_OK) throw Error{rc, dare_last_error()};
+    pt.mark("accumulate");
     rc = dare_scalar_from_sums(origin, voxel_size, dims, (const uint64_t*)acc.ptr,
                                (const uint64_t*)(acc.ptr + ncells), out);
     if (rc != DARE_OK) throw Error{rc, dare_last_error()};
+    pt.mark("finalize");
   });
 }
 

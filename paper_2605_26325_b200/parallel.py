@@ -147,7 +147,10 @@ class CudaOps:
         return px, cov
 
     @staticmethod
-    def compound_partial(sweep, plan, start, end, origin, voxel, dims):
+    def compound_partial(sweep, plan, start, end, origin, voxel, dims, stream=0):
+        """u64 sums/counts of frames [start, end) (torch (2, ncells) int64 on the
+        current device).  With a non-zero `stream` (cudaStream_t as int, the torch
+        current stream) nothing synchronises."""
         import torch
 
         from .reconstruct import frames_arg
@@ -164,7 +167,7 @@ class CudaOps:
                   _lib.ptr(idx, ctypes.c_int32), int(end - start), _lib.ptr(axes, ctypes.c_double),
                   plan.pixel_pitch[0], plan.pixel_pitch[1], _lib.ptr(mask, ctypes.c_uint8),
                   _lib.ptr(o, ctypes.c_double), float(voxel), _lib.ptr(d, ctypes.c_int64),
-                  ctypes.c_void_p(acc[0].data_ptr()), ctypes.c_void_p(acc[1].data_ptr()), ctypes.c_void_p(0))
+                  ctypes.c_void_p(acc[0].data_ptr()), ctypes.c_void_p(acc[1].data_ptr()), ctypes.c_void_p(stream))
         return acc
 
     @staticmethod
