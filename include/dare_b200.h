@@ -83,8 +83,13 @@ typedef struct {
   int64_t rejected_out_of_bounds;
   /* device pointers (read-only views, owned by the handle) */
   const uint32_t* d_cell_offsets; /* ncells + 1 exclusive prefix of counts */
-  const void* d_records;          /* n_samples x 16 B: f32 x,y,z, u32 (oid<<8 | intensity) */
+  const void* d_records;          /* n_samples x 16 B: f32 x,y,z, u32 (oid<<8 | intensity),
+                                     per cell grouped by z quarter (see d_bins / d_perm) */
   const float* d_orientations;    /* n_orientations x 4 f32 (w,x,y,z), canonical */
+  const uint32_t* d_bins;         /* ncells: z-quarter bin bounds (b1 | b2<<8 | b3<<16 | 1<<24)
+                                     of cells stored grouped by z quarter, 0 otherwise */
+  const int8_t* d_perm;           /* n_samples: the cell's j-th sample in insertion order
+                                     (index J = offsets[c] + j) is stored at J + perm[J] */
   size_t device_bytes;
 } dare_volume_info;
 
@@ -141,7 +146,8 @@ int dare_volume_seal(const double* origin, double voxel_size, const int64_t* dim
  * volumes built by dare_reconstruct over consecutive frame blocks into the
  * SAME grid.  Parts are given as device buffers on the current device (the
  * d_* views of dare_volume_info, or the same arrays received through NCCL):
- * per part the ncells+1 offsets, the 16 B records, the orientation table and
+ * per part the ncells+1 offsets, the 16 B records IN INSERTION ORDER (a
+ * handle's d_records read through its d_perm), the orientation table and
  * its sizes.  Within each cell the parts' runs are concatenated in part
  * order, which is the reference's insertion order when part r holds frames
  * after part r-1 -- the result is bit-identical to a single-device build. */

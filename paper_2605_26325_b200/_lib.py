@@ -50,6 +50,7 @@ class VolumeInfo(ctypes.Structure):
         ("origin", c_f64 * 3), ("voxel_size", c_f64), ("dims", c_i64 * 3),
         ("n_samples", c_i64), ("n_orientations", c_i64), ("rejected_out_of_bounds", c_i64),
         ("d_cell_offsets", c_vp), ("d_records", c_vp), ("d_orientations", c_vp),
+        ("d_bins", c_vp), ("d_perm", c_vp),
         ("device_bytes", c_sz),
     ]
 

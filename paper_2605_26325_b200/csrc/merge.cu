@@ -9,7 +9,9 @@
 //               orientation id rebased into the concatenated orientation table.
 // The parts are device buffers on the calling device (the local volume plus
 // buffers received through NCCL all-gather, or several local partial volumes
-// when the ranks are emulated on one GPU in tests).
+// when the ranks are emulated on one GPU in tests), records in insertion
+// order (a handle's storage order read through its perm); the merged volume is
+// z-binned like every other (volume.cuh).
 #include <cub/device/device_scan.cuh>
 
 #include <memory>
@@ -127,6 +129,7 @@ extern "C" int dare_volume_merge(const double* origin, double voxel_size, const 
     merge_copy_k<<<ceil_div(ncells * 32, 256), 256, 0, s>>>(parts, ncells, vol->d_offsets,
                                                              vol->d_records);
     DARE_CUDA(cudaGetLastError());
+    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     *out = vol.release();
   });

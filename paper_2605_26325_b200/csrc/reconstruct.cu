@@ -434,6 +434,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
         frame_scatter_k<false><<<grid, 256, 0, s>>>(fv, m, counts, offsets, keys, rej);
     };
     build_csr(vol.get(), FrameRecords{fv}, scatter, s);
+    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
     *out = vol.release();
@@ -482,6 +483,7 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
                                                                          offsets, keys, rej);
     };
     build_csr(vol.get(), SampleRecords{d_pos.ptr, d_word.ptr}, scatter, s);
+    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     *out = vol.release();
   });

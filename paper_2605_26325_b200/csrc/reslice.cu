@@ -56,6 +56,8 @@ constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fas
 struct ResliceArgs {
   const uint32_t* offsets;
   const uint4* records;
+  const uint32_t* bins;  // z-quarter bin bounds per cell (volume.cuh)
+  const int8_t* perm;    // insertion order -> storage order
   const double* params;  // P x 14
   const double* gate;    // P x n_orient (A, or +inf when rejected)
   const float* gate2;    // P x n_orient: f32(A * log2 e), +inf when rejected
@@ -295,12 +297,12 @@ __device__ __forceinline__ void exact_sums(Walk& w, const ResliceArgs& a, const 
   iwsum = 0.0;
   while (true) {
     while (w.live && mask == 0) {
+      // runs are in insertion (canonical) indices; storage through perm
       const uint32_t n = min(4u, w.e - w.s);
-      const uint4* __restrict__ q = a.records + w.s;
-      r0 = __ldg(q);
-      if (n > 1) r1 = __ldg(q + 1);
-      if (n > 2) r2 = __ldg(q + 2);
-      if (n > 3) r3 = __ldg(q + 3);
+      r0 = __ldg(a.records + canon_to_store(a.perm, w.s));
+      if (n > 1) r1 = __ldg(a.records + canon_to_store(a.perm, w.s + 1));
+      if (n > 2) r2 = __ldg(a.records + canon_to_store(a.perm, w.s + 2));
+      if (n > 3) r3 = __ldg(a.records + canon_to_store(a.perm, w.s + 3));
       w.s += n;
       mask = (keep(r0) ? 1u : 0u) | ((n > 1 && keep(r1)) ? 2u : 0u) | ((n > 2 && keep(r2)) ? 4u : 0u) |
              ((n > 3 && keep(r3)) ? 8u : 0u);
@@ -335,7 +337,7 @@ __device__ __forceinline__ void exact_sums_warp(Walk& w, const ResliceArgs& a, c
       bool k = false;
       double wt = 0.0, wi = 0.0;
       if (i < w.e) {
-        const uint4 c = __ldg(a.records + i);
+        const uint4 c = __ldg(a.records + canon_to_store(a.perm, i));
         k = w.in_cube(c) && gate[c.w >> 8] != CUDART_INF;
         if (k) {
           wt = exact_weight<kDistMode>(a, w, c, gate);
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
 struct FastWalk {
   float xlo, xhi, ylo, yhi, zlo, zhi;
   int lox, hix, loy, hiy, loz, hiz, cx, cy, jx, jy;
+  int blo, bhi;  // first z quarter of cell loz / last z quarter of cell hiz that can hold a survivor
   uint32_t s, e;
 
   // Columns in phases (cx mod 3, cy mod 3): within a phase, the 3x3
@@ -404,9 +407,15 @@ struct FastWalk {
     while (jx < 3) {
       while (cx <= hix) {
         while (cy <= hiy) {
+          // one contiguous storage range: drop the z quarters of the first and
+          // last cell that lie wholly outside [zlo, zhi] (binned cells only)
           const int64_t base = ((int64_t)cx * a.dims[1] + cy) * a.dims[2];
-          s = __ldg(a.offsets + base + loz);
-          e = __ldg(a.offsets + base + hiz + 1);
+          const uint32_t o_lo = __ldg(a.offsets + base + loz);
+          const uint32_t o_hi = __ldg(a.offsets + base + hiz);
+          const uint32_t o_end = __ldg(a.offsets + base + hiz + 1);
+          const uint32_t w_lo = __ldg(a.bins + base + loz), w_hi = __ldg(a.bins + base + hiz);
+          s = o_lo + ((w_lo >> 24) ? bin_start(w_lo, blo) : 0u);
+          e = ((w_hi >> 24) && bhi < 3) ? o_hi + bin_start(w_hi, bhi + 1) : o_end;
           cy += 3;
           if (s < e) {
             visits += e - s;
@@ -501,9 +510,9 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 
 // Certified path: same mapping as reslice_k; branch-free f32 weights for
 // every visited record (no warp rounds), 4 loads in flight, phased walk.
-template <int kDistMode, bool kSmemGate>
-__global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
-                                                      uint8_t* __restrict__ cov) {
+template <int kDistMode, bool kSmemGate, int kB = 4, int kMinBlocks = 4>
+__global__ void __launch_bounds__(256, kMinBlocks) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
+                                                               uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
@@ -547,25 +556,30 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     w.cy = w.loy + (3 - w.loy % 3) % 3;
     w.s = w.e = 0;
     live = active && w.lox <= w.hix && w.loy <= w.hiy && w.loz <= w.hiz;
+    // quarters of cell loz below zlo and of cell hiz above zhi hold no survivor:
+    // bin b holds zb(b) <= z < zb(b+1), so b < blo => z < zb(blo) <= zlo, and
+    // b > bhi => z >= zb(bhi+1) > zhi (exact f32 comparisons).
+    w.blo = w.bhi = 0;
+    for (int k = 1; k <= 3; ++k) {
+      w.blo += zbin_bound(a.origin[2], a.voxel, w.loz, k) <= w.zlo;
+      w.bhi += zbin_bound(a.origin[2], a.voxel, w.hiz, k) <= w.zhi;
+    }
   }
   uint32_t visits = 0;
   if (live) live = w.open(a, visits);
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
   while (live) {
-    const uint32_t n = min(4u, w.e - w.s);
+    const uint32_t n = min((uint32_t)kB, w.e - w.s);
     const uint4* __restrict__ q = a.records + w.s;
     // unconditional loads (clamped to the run): no branches around them
-    const uint4 r0 = __ldg(q);
-    const uint4 r1 = __ldg(q + min(1u, n - 1));
-    const uint4 r2 = __ldg(q + min(2u, n - 1));
-    const uint4 r3 = __ldg(q + min(3u, n - 1));
+    uint4 r[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) r[i] = __ldg(q + min((uint32_t)i, n - 1));
     w.s += n;
     float bw = 0.0f, bj = 0.0f;
-    fast_term<kDistMode, kSmemGate>(r0, true, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode, kSmemGate>(r1, n > 1, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode, kSmemGate>(r2, n > 2, w, gate, wh, wl, c2, bw, bj);
-    fast_term<kDistMode, kSmemGate>(r3, n > 3, w, gate, wh, wl, c2, bw, bj);
+#pragma unroll
+    for (int i = 0; i < kB; ++i) fast_term<kDistMode, kSmemGate>(r[i], i == 0 || (uint32_t)i < n, w, gate, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
     if (w.s == w.e) live = w.open(a, visits);
@@ -718,6 +732,16 @@ static double certified_lambda(const dare_reslice_cfg& c) {
   return kLn2 * (9.0 * kEps32 + kRsqErr + 16.0 * kEps64) * M + 1.01 * kEx2Err + 3.0 * kEps64;
 }
 
+// Development aid: DARE_FAST_VARIANT selects a batch-size / occupancy variant
+// of the certified kernel (profiling experiments only; 0 = default).
+static int fast_variant() {
+  static const int v = [] {
+    const char* e = getenv("DARE_FAST_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <class K>
 static void set_smem(K kernel) {
   DARE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -735,6 +759,8 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   ResliceArgs a;
   a.offsets = vol->d_offsets;
   a.records = vol->d_records;
+  a.bins = vol->d_bins;
+  a.perm = vol->d_perm;
   a.params = d_params;
   a.n_orient = std::max<int64_t>(vol->n_orient, 1);
   for (int i = 0; i < 3; ++i) {
@@ -800,6 +826,10 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_fast_k<0, false>);
     set_smem(reslice_fast_k<2, true>);
     set_smem(reslice_fast_k<2, false>);
+    set_smem(reslice_fast_k<0, true, 4, 5>);
+    set_smem(reslice_fast_k<0, true, 8, 3>);
+    set_smem(reslice_fast_k<0, true, 8, 4>);
+    set_smem(reslice_fast_k<0, true, 2, 5>);
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -823,6 +853,14 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   const bool smem_gate = !a.pose_major && a.n_orient <= kGateSmemF;
   if (a.dist_mode == 2)
     (smem_gate ? reslice_fast_k<2, true> : reslice_fast_k<2, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else if (smem_gate && fast_variant() == 1)
+    reslice_fast_k<0, true, 4, 5><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else if (smem_gate && fast_variant() == 2)
+    reslice_fast_k<0, true, 8, 3><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else if (smem_gate && fast_variant() == 3)
+    reslice_fast_k<0, true, 8, 4><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  else if (smem_gate && fast_variant() == 4)
+    reslice_fast_k<0, true, 2, 5><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   else
     (smem_gate ? reslice_fast_k<0, true> : reslice_fast_k<0, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");

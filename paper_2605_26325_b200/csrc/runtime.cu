@@ -160,6 +160,8 @@ dare_volume_s::~dare_volume_s() {
   dev_free(d_offsets);
   dev_free(d_records);
   dev_free(d_orient);
+  dev_free(d_bins);
+  dev_free(d_perm);
   cudaSetDevice(prev);
 }
 

@@ -7,7 +7,19 @@
 //   offsets  u32[ncells+1]   exclusive prefix of cell counts
 //   records  uint4[n]        {f32 x, f32 y, f32 z, u32 (oid << 8) | intensity}
 //   orients  float4[n_oid]   distinct canonical f32 quaternions (w,x,y,z)
+//   bins     u32[ncells]      z-quarter bin bounds of the cell (see below)
+//   perm     i8[n]            reference (insertion) order -> storage order
 // Positions stay bit-identical f32 (the reslice cube test needs them exactly).
+//
+// z-binning: within every cell of <= 32 samples the run is stored stably
+// grouped by z quarter (bin b holds zb(iz, b) <= z < zb(iz, b+1), zb below),
+// so a reslice column walk can drop the quarters of its first and last z-cell
+// that lie outside the pixel's cube and still read ONE contiguous range.
+// bins[c] = b1 | b2 << 8 | b3 << 16 | 1 << 24 with bk = #samples in bins < k
+// (bit 24 clear: cell kept in insertion order).  The reference's insertion
+// order is recovered through perm: the cell's j-th sample in insertion order,
+// canonical index J = off[c] + j, is stored at J + perm[J].  Exact consumers
+// (FP64 reslice path, brute force, download, merge) read through perm.
 // Quaternions are deduplicated: every sample of a reconstructed frame shares
 // the frame's quaternion (reconstruct.py:192-196), so oid = frame slot and the
 // per-pose orientation gates are evaluated once per oid, not per sample.
@@ -28,6 +40,8 @@ struct dare_volume_s {
   uint32_t* d_offsets = nullptr;
   uint4* d_records = nullptr;
   float4* d_orient = nullptr;
+  uint32_t* d_bins = nullptr;
+  int8_t* d_perm = nullptr;
   ~dare_volume_s();
 };
 
@@ -44,6 +58,27 @@ struct dare_scalar_s {
 };
 
 namespace dare {
+
+constexpr int kMaxBinnedRun = 32;  // cells with more samples stay in insertion order
+
+// z-bin boundary k (1..3) of cell row iz: f32(origin_z + (iz + k/4) * voxel).
+__device__ __forceinline__ float zbin_bound(double oz, double voxel, int64_t iz, int k) {
+  return __double2float_rn(oz + ((double)iz + 0.25 * k) * voxel);
+}
+
+// Number of samples of a binned cell in bins < b (b = 0..3); bins word w.
+__device__ __forceinline__ uint32_t bin_start(uint32_t w, int b) {
+  return b == 0 ? 0u : (w >> (8 * (b - 1))) & 0xffu;
+}
+
+// Canonical (insertion-order) index -> storage index.
+__device__ __forceinline__ uint32_t canon_to_store(const int8_t* __restrict__ perm, uint32_t j) {
+  return j + (int32_t)__ldg(perm + j);
+}
+
+// Groups every cell of <= kMaxBinnedRun samples by z quarter in place (stable),
+// allocates and fills d_bins / d_perm.  Input: records in insertion order.
+void bin_volume(dare_volume_s* vol, cudaStream_t s);
 
 VoxelMap make_voxel_map(const double* origin, double voxel, const int64_t* dims);
 

@@ -126,6 +126,7 @@ extern "C" int dare_volume_upload(const double* origin, double voxel_size, const
     if (!table.empty())
       DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
                                 cudaMemcpyHostToDevice, s));
+    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     *out = vol.release();
   });
@@ -140,11 +141,14 @@ extern "C" int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int
     std::vector<uint32_t> offsets(vol->ncells + 1);
     std::vector<uint4> records((size_t)vol->n_samples);
     std::vector<float4> table((size_t)vol->n_orient);
+    std::vector<int8_t> perm((size_t)vol->n_samples);
     DARE_CUDA(cudaMemcpyAsync(offsets.data(), vol->d_offsets, sizeof(uint32_t) * offsets.size(),
                               cudaMemcpyDeviceToHost, s));
-    if (!records.empty())
+    if (!records.empty()) {
       DARE_CUDA(cudaMemcpyAsync(records.data(), vol->d_records, sizeof(uint4) * records.size(),
                                 cudaMemcpyDeviceToHost, s));
+      DARE_CUDA(cudaMemcpyAsync(perm.data(), vol->d_perm, perm.size(), cudaMemcpyDeviceToHost, s));
+    }
     if (!table.empty())
       DARE_CUDA(cudaMemcpyAsync(table.data(), vol->d_orient, sizeof(float4) * table.size(),
                                 cudaMemcpyDeviceToHost, s));
@@ -153,8 +157,8 @@ extern "C" int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int
       if (cell_starts) cell_starts[c] = offsets[c];
       if (cell_counts) cell_counts[c] = (int64_t)offsets[c + 1] - offsets[c];
     }
-    for (int64_t i = 0; i < vol->n_samples; ++i) {
-      const uint4& r = records[i];
+    for (int64_t i = 0; i < vol->n_samples; ++i) {  // insertion order through perm
+      const uint4& r = records[i + perm[i]];
       if (positions) std::memcpy(positions + 3 * i, &r, 12);
       if (orientations) std::memcpy(orientations + 4 * i, &table[r.w >> 8], 16);
       if (intensities) intensities[i] = (uint8_t)(r.w & 0xffu);
@@ -178,7 +182,9 @@ extern "C" int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info) {
     info->d_cell_offsets = vol->d_offsets;
     info->d_records = vol->d_records;
     info->d_orientations = (const float*)vol->d_orient;
-    info->device_bytes = sizeof(uint32_t) * (vol->ncells + 1) + sizeof(uint4) * vol->n_samples +
+    info->d_bins = vol->d_bins;
+    info->d_perm = vol->d_perm;
+    info->device_bytes = sizeof(uint32_t) * (2 * vol->ncells + 1) + (sizeof(uint4) + 1) * vol->n_samples +
                          sizeof(float4) * vol->n_orient;
   });
 }

@@ -113,16 +113,26 @@ class CudaOps:
         nc = int(np.prod(info.dims))
         n, no = int(info.n_samples), int(info.n_orientations)
         offs = torch.as_tensor(_CudaArray(info.d_cell_offsets, (nc + 1,), "<i4"), device="cuda")
-        recs = torch.as_tensor(_CudaArray(info.d_records, (n, 4), "<i4"), device="cuda") if n else \
-            torch.zeros((0, 4), dtype=torch.int32, device="cuda")
+        if n:  # records in insertion order: storage index = J + perm[J]
+            store = torch.as_tensor(_CudaArray(info.d_records, (n, 4), "<i4"), device="cuda")
+            perm = torch.as_tensor(_CudaArray(info.d_perm, (n,), "|i1"), device="cuda")
+            recs = store[torch.arange(n, device="cuda") + perm.long()]
+        else:
+            recs = torch.zeros((0, 4), dtype=torch.int32, device="cuda")
         oris = torch.as_tensor(_CudaArray(info.d_orientations, (no, 4), "<f4"), device="cuda") if no else \
             torch.zeros((0, 4), dtype=torch.float32, device="cuda")
+        torch.cuda.current_stream().synchronize()  # the library reads these on its own stream
         return Part(offs, recs, oris, n, no, int(info.rejected_out_of_bounds))
 
     @staticmethod
     def merge(parts: list[Part], origin, voxel, dims):
+        import torch
+
         from .volume import DirectionalVolume, _Handle
 
+        # parts may come from torch kernels / NCCL on torch's stream; the merge
+        # runs on the library's per-thread stream
+        torch.cuda.current_stream().synchronize()
         k = len(parts)
         offs = (ctypes.c_void_p * k)(*[p.offsets.data_ptr() for p in parts])
         recs = (ctypes.c_void_p * k)(*[p.records.data_ptr() if p.n_samples else 0 for p in parts])
@@ -157,6 +167,8 @@ class CudaOps:
 
         nc = int(np.prod(dims))
         acc = torch.zeros((2, nc), dtype=torch.int64, device="cuda")
+        if not stream:  # the library's own stream does not order after torch's zero fill
+            torch.cuda.current_stream().synchronize()
         images, frames_ptr, on_device = frames_arg(sweep)
         idx = np.ascontiguousarray(plan.image_index[start:end])
         axes = np.ascontiguousarray(plan.axes()[start:end])
@@ -172,7 +184,11 @@ class CudaOps:
 
     @staticmethod
     def scalar_from_sums(acc, origin, voxel, dims):
+        import torch
+
         from .scalar import ScalarVolume
+
+        torch.cuda.current_stream().synchronize()  # acc may come from an all-reduce on torch's stream
 
         o = np.ascontiguousarray(origin, dtype=np.float64)
         d = np.ascontiguousarray(dims, dtype=np.int64)

@@ -26,6 +26,11 @@ def frames_arg(sweep, frames_device_ptr: int | None = None):
     if frames_device_ptr is None and getattr(images, "is_cuda", False):
         if images.dtype.itemsize != 1 or not images.is_contiguous():
             raise InvalidArgumentError("device images must be a contiguous uint8 tensor")
+        import torch
+
+        # the library reads the frames on its own (non-blocking) stream: finish
+        # whatever torch work produced them first
+        torch.cuda.current_stream(images.device).synchronize()
         frames_device_ptr = images.data_ptr()
     if frames_device_ptr is not None:
         return images, ctypes.c_void_p(int(frames_device_ptr)), 1

@@ -396,3 +396,40 @@ def test_half_integer_ties_take_the_exact_fallback(rng, k_dist):
                              cfg.unassigned_value)
         np.testing.assert_array_equal(fa[0][k], ref[0], err_msg=f"plane {k}")
         np.testing.assert_array_equal(fa[1][k].astype(bool), ref[1], err_msg=f"plane {k}")
+
+
+def test_z_binned_layout_round_trips_every_run_length():
+    """Cells of 1..40 samples inserted in descending z (so z-quarter binning
+    permutes every binned cell): the device layout regroups cells of <= 32
+    samples by quarter, and download / reslice still see insertion order."""
+    import torch
+
+    from paper_2605_26325_b200.parallel import _CudaArray
+
+    pos, inten = [], []
+    for c in range(40):
+        for j in range(c + 1):
+            pos.append((c + 0.5, 0.5, 0.99 - j * 0.98 / (c + 1)))
+            inten.append((7 * j + c) % 256)
+    pos = np.array(pos)
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (40, 1, 1)), 1.0)
+    b.insert_batch(pos, np.tile([1.0, 0, 0, 0], (len(pos), 1)), np.array(inten))
+    v = b.seal()
+    np.testing.assert_array_equal(np.asarray(v.positions), pos.astype(np.float32))
+    np.testing.assert_array_equal(np.asarray(v.intensities), np.array(inten, np.uint8))
+    info = v.device_info()
+    counts = np.asarray(v.cell_counts)
+    bins = torch.as_tensor(_CudaArray(info.d_bins, (len(counts),), "<u4"), device="cuda").cpu().numpy()
+    perm = torch.as_tensor(_CudaArray(info.d_perm, (int(info.n_samples),), "|i1"), device="cuda").cpu().numpy()
+    for c in np.nonzero(counts)[0]:
+        binned = bool(bins[c] >> 24)
+        assert binned == (counts[c] <= 32), c
+        if binned and counts[c] > 1:
+            assert (perm[v.cell_starts[c]:v.cell_starts[c] + counts[c]] != 0).any()
+    # reslice through the binned layout == oracle on the reference layout
+    plane = ReslicePlane(Pose(Quaternion.identity(), (0.3, 0.5, 0.4)), 40, 1, (1.0, 1.0))
+    cfg = ResliceConfig(interp_radius=0.6, k_dist=2.0)
+    got = db.reslice(v, plane, cfg)
+    ref = oracle.reslice(v, oracle.plane_params(plane), oracle.cfg_array(cfg), 40, 1, 0)
+    np.testing.assert_array_equal(got.pixels, ref[0])
+    np.testing.assert_array_equal(got.coverage, ref[1])
