@@ -247,11 +247,11 @@ int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream);
  * inconclusive (0 with cfg.exact = 1, or when the fast path is disabled). */
 int dare_reslice_last_fallback(int64_t* n_pixels);
 /* Exhaustive check (every f32 input of the ranges the certified reslice path
- * uses) of the hardware ex2.approx / rsqrt.approx relative error on the
+ * uses) of the hardware ex2.approx / sqrt.approx relative error on the
  * current device; *ok = 1 when both are within the constants the bound
  * assumes.  The fast path runs this once per device and disables itself
  * (exact FP64 for every pixel) if it fails. */
-int dare_fastmath_check(double* ex2_max_rel_err, double* rsqrt_max_rel_err, int32_t* ok);
+int dare_fastmath_check(double* ex2_max_rel_err, double* sqrt_max_rel_err, int32_t* ok);
 
 #ifdef __cplusplus
 }

@@ -49,8 +49,8 @@ __global__ void __launch_bounds__(256) bin_cells_k(const uint32_t* __restrict__ 
       const uint32_t before = bin == 0 ? 0 : (bin == 1 ? c1 : (bin == 2 ? c2 : c3));
       const uint32_t dest = before + __popc(m[bin] & ((1u << hl) - 1u));
       __syncwarp();
-      if (mine) {
-        records[s + dest] = rec;
+      if (mine) {  // sweeps mostly insert a cell's samples in z order: skip unmoved records
+        if (dest != (uint32_t)hl) records[s + dest] = rec;
         perm[s + hl] = (int8_t)((int)dest - hl);
       }
       if (small && hl == 0) bins[c0] = c1 | (c2 << 8) | (c3 << 16) | (1u << 24);
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) bin_cells_k(const uint32_t* __restrict__ 
       const uint32_t dest = before + __popc(m[bin] & ((1u << lane) - 1u));
       __syncwarp();
       if (mine) {
-        records[cs + dest] = rec;
+        if (dest != (uint32_t)lane) records[cs + dest] = rec;
         perm[cs + lane] = (int8_t)((int)dest - lane);
       }
       if (lane == 0) bins[c] = c1 | (c2 << 8) | (c3 << 16) | (1u << 24);

@@ -12,7 +12,7 @@
 //   order per pixel (thread per pixel, same walk);
 // * certified (reslice_fast_k, default): the SAME survivor set (exact cube and
 //   gate tests), but each weight is evaluated in f32 with the hardware ex2 /
-//   rsqrt approximations and the sums carry a rigorous relative error bound
+//   sqrt approximations and the sums carry a rigorous relative error bound
 //   (derivation at certify()).  Because the output is a rounded u8 and a
 //   threshold test, the bound decides the reference's result for all but a
 //   tiny fraction of pixels; those are appended to a list and recomputed by
@@ -50,7 +50,7 @@ constexpr double kEps64 = 1.1102230246251565e-16;   // 2^-53
 // Relative-error constants the certified bound assumes for the hardware
 // approximations; dare_fastmath_check verifies them exhaustively per device.
 constexpr double kEx2Err = 4.76837158203125e-07;    // 2^-21
-constexpr double kRsqErr = 4.76837158203125e-07;    // 2^-21
+constexpr double kSqrtErr = 4.76837158203125e-07;   // 2^-21
 constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fast path accepts
 
 struct ResliceArgs {
@@ -156,9 +156,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-__device__ __forceinline__ float rsqrt_approx(float x) {
+__device__ __forceinline__ float sqrt_approx(float x) {
   float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -455,7 +455,7 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
     const float dy = __fsub_rn(__fsub_rn(__uint_as_float(c.y), wh[1]), wl[1]);
     const float dz = __fsub_rn(__fsub_rn(__uint_as_float(c.z), wh[2]), wl[2]);
     const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-    const float dist = __fmul_rn(d2, rsqrt_approx(fmaxf(d2, 1e-30f)));
+    const float dist = sqrt_approx(d2);  // subnormal d2 flushes: |error| < 1.1e-19 (abs slack)
     arg = __fmaf_rn(-dist, c2, g);
   }
   const float wt = k ? ex2_approx(arg) : 0.0f;
@@ -470,7 +470,7 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
 //  (1) Per survivor, |ln(w_hat_i / w_i)| <= lam (host part a.lam, see
 //      certified_lambda(), plus the pixel-position term below), from: two-float
 //      pixel position (dx error <= 2.01 e32 |dx| + 2.01 e32^2 |w|), f32 squares,
-//      rsqrt.approx (kRsqErr), f32 gate A2 and scale c2 (one rounding each),
+//      sqrt.approx (kSqrtErr), f32 gate A2 and scale c2 (one rounding each),
 //      the FMA exponent, ex2.approx (kEx2Err), the reference's own FP64 chain
 //      (<= 16 e64 M) and glibc exp (<= 2 e64).
 //  (2) Batch sums of <= 4 non-negative f32 terms: bw <= 3 roundings, bj <= 4
@@ -651,7 +651,7 @@ __global__ void exp_k(const double* x, double* y, int64_t n) {
 }
 
 // ---- hardware approximation check ----------------------------------------
-// Max relative error of ex2.approx (which = 0) or rsqrt.approx (which = 1)
+// Max relative error of ex2.approx (which = 0) or sqrt.approx (which = 1)
 // over the f32 bit patterns [lo, lo + count), against FP64 references; a NaN
 // or infinite error counts as 1.  Non-negative doubles order like their bits.
 __global__ void mufu_check_k(int which, uint32_t lo, uint64_t count, unsigned long long* maxerr) {
@@ -664,8 +664,8 @@ __global__ void mufu_check_k(int which, uint32_t lo, uint64_t count, unsigned lo
       got = (double)ex2_approx(x);
       ref = exp2((double)x);
     } else {
-      got = (double)rsqrt_approx(x);
-      ref = 1.0 / sqrt((double)x);
+      got = (double)sqrt_approx(x);
+      ref = sqrt((double)x);
     }
     double err = fabs(got - ref) / ref;
     if (!(err <= 1.0)) err = 1.0;
@@ -688,8 +688,9 @@ static void fastmath_measure(cudaStream_t s, double* ex2_err, double* rsq_err) {
   const uint32_t top = bits((float)kMaxLog2Arg);
   mufu_check_k<<<grid, 256, 0, s>>>(0, 0u, (uint64_t)top + 1, d.ptr);
   mufu_check_k<<<grid, 256, 0, s>>>(0, 0x80000000u, (uint64_t)top + 1, d.ptr);
-  // rsqrt on every finite f32 >= 1e-30 (the clamp floor of d2)
-  const uint32_t lo = bits(1e-30f);
+  // sqrt on every finite normal f32 (subnormal inputs flush to 0: absolute error
+  // < 1.1e-19, inside the bound's absolute slack)
+  const uint32_t lo = bits(1.17549435e-38f);
   mufu_check_k<<<grid, 256, 0, s>>>(1, lo, (uint64_t)0x7f7fffffu - lo + 1, d.ptr + 1);
   DARE_CUDA(cudaGetLastError());
   unsigned long long h[2];
@@ -710,7 +711,7 @@ static bool fastmath_ok(cudaStream_t s) {
   if (state[dev] == 0) {
     double e1 = 1.0, e2 = 1.0;
     fastmath_measure(s, &e1, &e2);
-    state[dev] = (e1 <= kEx2Err && e2 <= kRsqErr) ? 1 : -1;
+    state[dev] = (e1 <= kEx2Err && e2 <= kSqrtErr) ? 1 : -1;
   }
   return state[dev] == 1;
 }
@@ -729,7 +730,7 @@ static double certified_lambda(const dare_reslice_cfg& c) {
   const double M = (kLog2e * (fabs(c.k_normal) * span(c.cos_normal) + fabs(c.k_inplane) * span(c.cos_inplane) +
                               fabs(c.k_dist) * 1.7320508075688774) * (1.0 + 1e-9)) + 1e-9;
   if (!(M <= kMaxLog2Arg - 1.0)) return -1.0;
-  return kLn2 * (9.0 * kEps32 + kRsqErr + 16.0 * kEps64) * M + 1.01 * kEx2Err + 3.0 * kEps64;
+  return kLn2 * (9.0 * kEps32 + kSqrtErr + 16.0 * kEps64) * M + 1.01 * kEx2Err + 3.0 * kEps64;
 }
 
 // Development aid: DARE_FAST_VARIANT selects a batch-size / occupancy variant
@@ -963,13 +964,13 @@ extern "C" int dare_reslice_last_fallback(int64_t* n_pixels) {
   });
 }
 
-extern "C" int dare_fastmath_check(double* ex2_max_rel_err, double* rsqrt_max_rel_err, int32_t* ok) {
+extern "C" int dare_fastmath_check(double* ex2_max_rel_err, double* sqrt_max_rel_err, int32_t* ok) {
   return guard([&] {
     double e1 = 1.0, e2 = 1.0;
     fastmath_measure(thread_stream(), &e1, &e2);
     if (ex2_max_rel_err) *ex2_max_rel_err = e1;
-    if (rsqrt_max_rel_err) *rsqrt_max_rel_err = e2;
-    if (ok) *ok = (e1 <= kEx2Err && e2 <= kRsqErr) ? 1 : 0;
+    if (sqrt_max_rel_err) *sqrt_max_rel_err = e2;
+    if (ok) *ok = (e1 <= kEx2Err && e2 <= kSqrtErr) ? 1 : 0;
   });
 }
 

@@ -332,13 +332,13 @@ def _reslice_raw(vol, planes, cfg, exact, schedule=0):
 
 
 def test_fastmath_constants_hold_exhaustively():
-    """Every f32 input of ex2.approx / rsqrt.approx in the ranges the certified
+    """Every f32 input of ex2.approx / sqrt.approx in the ranges the certified
     bound uses is within the assumed 2^-21 relative error on this device."""
     import ctypes
 
     e1, e2, ok = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
     _lib.call("dare_fastmath_check", ctypes.byref(e1), ctypes.byref(e2), ctypes.byref(ok))
-    print(f"ex2.approx max rel err {e1.value:.3e}, rsqrt.approx max rel err {e2.value:.3e}")
+    print(f"ex2.approx max rel err {e1.value:.3e}, sqrt.approx max rel err {e2.value:.3e}")
     assert ok.value == 1
     assert 0 < e1.value <= 2.0 ** -21 and 0 < e2.value <= 2.0 ** -21
 
