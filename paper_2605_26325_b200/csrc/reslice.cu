@@ -156,6 +156,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 32 B load of records 2p, 2p+1 (256-bit LDG; records base is 32 B aligned).
+__device__ __forceinline__ void load_pair(const uint4* __restrict__ rec, uint32_t p, uint4& a, uint4& b) {
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(rec + 2 * (size_t)p));
+}
+
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -569,20 +576,25 @@ __global__ void __launch_bounds__(256, kMinBlocks) reslice_fast_k(ResliceArgs a,
   if (live) live = w.open(a, visits);
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
+  // batches of 4 record slots = 2 aligned pairs (256-bit loads); slots outside
+  // [s, e) (an odd run start, the run end) are masked
+  uint32_t i0 = w.s & ~1u;
   while (live) {
-    const uint32_t n = min((uint32_t)kB, w.e - w.s);
-    const uint4* __restrict__ q = a.records + w.s;
-    // unconditional loads (clamped to the run): no branches around them
-    uint4 r[kB];
-#pragma unroll
-    for (int i = 0; i < kB; ++i) r[i] = __ldg(q + min((uint32_t)i, n - 1));
-    w.s += n;
+    uint4 r[4];
+    const uint32_t last_pair = (w.e - 1) >> 1;
+    load_pair(a.records, i0 >> 1, r[0], r[1]);
+    load_pair(a.records, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
     float bw = 0.0f, bj = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kB; ++i) fast_term<kDistMode, kSmemGate>(r[i], i == 0 || (uint32_t)i < n, w, gate, wh, wl, c2, bw, bj);
+    for (int i = 0; i < 4; ++i)
+      fast_term<kDistMode, kSmemGate>(r[i], i0 + i >= w.s && i0 + i < w.e, w, gate, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
-    if (w.s == w.e) live = w.open(a, visits);
+    i0 += 4;
+    if (i0 >= w.e) {
+      live = w.open(a, visits);
+      i0 = w.s & ~1u;
+    }
   }
   if (!active) return;
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
