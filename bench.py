@@ -562,7 +562,7 @@ def run_b200(args):
         main_kernel = f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>"
     else:
         smem_gate = schedule == 1 and int(info.n_orientations) <= 1024
-        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {1 if smem_gate else 0}, 4, 4>"
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {1 if smem_gate else 0}>"
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
     # [fallback kernel on the certified path]

@@ -517,9 +517,9 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 
 // Certified path: same mapping as reslice_k; branch-free f32 weights for
 // every visited record (no warp rounds), 4 loads in flight, phased walk.
-template <int kDistMode, bool kSmemGate, int kB = 4, int kMinBlocks = 4>
-__global__ void __launch_bounds__(256, kMinBlocks) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
-                                                               uint8_t* __restrict__ cov) {
+template <int kDistMode, bool kSmemGate>
+__global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
+                                                      uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
@@ -745,16 +745,6 @@ static double certified_lambda(const dare_reslice_cfg& c) {
   return kLn2 * (9.0 * kEps32 + kSqrtErr + 16.0 * kEps64) * M + 1.01 * kEx2Err + 3.0 * kEps64;
 }
 
-// Development aid: DARE_FAST_VARIANT selects a batch-size / occupancy variant
-// of the certified kernel (profiling experiments only; 0 = default).
-static int fast_variant() {
-  static const int v = [] {
-    const char* e = getenv("DARE_FAST_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <class K>
 static void set_smem(K kernel) {
   DARE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -839,10 +829,6 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_fast_k<0, false>);
     set_smem(reslice_fast_k<2, true>);
     set_smem(reslice_fast_k<2, false>);
-    set_smem(reslice_fast_k<0, true, 4, 5>);
-    set_smem(reslice_fast_k<0, true, 8, 3>);
-    set_smem(reslice_fast_k<0, true, 8, 4>);
-    set_smem(reslice_fast_k<0, true, 2, 5>);
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -866,14 +852,6 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   const bool smem_gate = !a.pose_major && a.n_orient <= kGateSmemF;
   if (a.dist_mode == 2)
     (smem_gate ? reslice_fast_k<2, true> : reslice_fast_k<2, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else if (smem_gate && fast_variant() == 1)
-    reslice_fast_k<0, true, 4, 5><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else if (smem_gate && fast_variant() == 2)
-    reslice_fast_k<0, true, 8, 3><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else if (smem_gate && fast_variant() == 3)
-    reslice_fast_k<0, true, 8, 4><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else if (smem_gate && fast_variant() == 4)
-    reslice_fast_k<0, true, 2, 5><<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   else
     (smem_gate ? reslice_fast_k<0, true> : reslice_fast_k<0, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");
