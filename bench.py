@@ -593,7 +593,8 @@ def run_b200(args):
         out = {
             "metric": "reslices/sec", "value": value, "unit": "reslices/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64" if args.exact else "f32 weights + f64 sums (certified, exact u8 output)",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> dims {dims} "
                                    f"({info.n_samples} samples), {B} poses/step at {W}x{H}, r={cfg.interp_radius}",
                        "poses_per_step": B, "parallelism": f"pose-sharded x{ws} (replicated volume)",
