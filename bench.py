@@ -56,6 +56,8 @@ def parse_args():
     p.add_argument("--batch", type=int, default=0, help="poses per step (default: config's)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-scalar", action="store_true", help="skip the direction-blind arm timings")
+    p.add_argument("--schedule", type=int, default=0, choices=[0, 1, 2],
+                   help="reslice schedule: 0 auto (as dare_reslice decides), 1 pixel-major, 2 pose-major")
     p.add_argument("--exact", action="store_true",
                    help="FP64 reference arithmetic for every pixel (default: certified f32 + exact fallback)")
     return p.parse_args()
@@ -481,7 +483,7 @@ def run_b200(args):
     p0 = params[args.warmup * B:(args.warmup + 1) * B]
     coherent = _lib.load().dare_poses_coherent(p0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B, W, H,
                                                float(wl.voxel))
-    schedule = 2 if coherent else 1
+    schedule = args.schedule or (2 if coherent and args.exact else 1)  # same rule as dare_reslice's auto
     kc = kernel_cfg(cfg, schedule, exact=args.exact)
     # a real (non-default) stream: the kernels and the timing events share it
     stream = torch.cuda.Stream()

@@ -63,8 +63,9 @@ typedef struct {
   double k_dist;
   int32_t unassigned;
   int32_t schedule; /* 0 auto, 1 pixel-major (spatially sorted batch), 2 pose-major
-                       (lanes = one pixel of 32 consecutive poses; for coherent
-                       trajectories).  Results are identical; only speed differs. */
+                       (lanes = one pixel of 32 consecutive poses; auto picks it for
+                       coherent trajectories on the exact path only).  Results are
+                       identical; only speed differs. */
   int32_t exact;    /* 0: certified f32 weights with exact-FP64 fallback for every
                        pixel whose u8 value / coverage the error bound cannot decide
                        (default); 1: FP64 reference arithmetic for every pixel.

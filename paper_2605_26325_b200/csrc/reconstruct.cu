@@ -191,6 +191,15 @@ struct FrameRecords {
     return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
                       (fv.oid[f] << 8) | (uint32_t)(key & 0xffu));
   }
+  // z only (the binning key), same arithmetic as operator()
+  __device__ __forceinline__ float z_of(unsigned long long key) const {
+    const uint32_t pid = (uint32_t)(key >> 8);
+    const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
+    const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
+    const double* fa = fv.axes + (size_t)f * 9;
+    const double U = (double)u * fv.px, V = (double)v * fv.py;
+    return __double2float_rn((U * fa[2] + V * fa[5]) + fa[8]);
+  }
 };
 
 struct SampleRecords {
@@ -201,6 +210,7 @@ struct SampleRecords {
     return make_uint4(__float_as_uint(pos[3 * i]), __float_as_uint(pos[3 * i + 1]),
                       __float_as_uint(pos[3 * i + 2]), word[i]);
   }
+  __device__ __forceinline__ float z_of(unsigned long long key) const { return pos[3 * (size_t)key + 2]; }
 };
 
 constexpr int kSmallRun = 32;  // per-cell runs sorted in shared memory by one lane
@@ -211,19 +221,33 @@ struct SealSmem {
   unsigned long long st[kSmallRun * kPitch];  // st[k * kPitch + lane] = k-th key of cell c0+lane
   uint16_t cstart[32];                         // cell start relative to the warp's first key
   uint8_t cell_of[kSmallRun * 32];             // key position -> lane of its cell (0xff: big run)
+  uint8_t slot[kSmallRun * 32];                // key position -> z bin, then destination in its cell
+};
+
+// z-quarter binning of the sealed runs (layout in volume.cuh)
+struct BinOut {
+  double oz, voxel;
+  int64_t nz;
+  uint32_t* bins;
+  int8_t* perm;
 };
 
 // Warp seals cells [c0, c0+32).  Keys are loaded coalesced into a transposed,
 // padded stage (cell = column), each lane insertion-sorts its column (runs are
 // ~16 keys; the padded pitch makes the lanes' row accesses bank-conflict
-// free), and the records are written back coalesced in storage order.  Runs
-// longer than kSmallRun are listed for the CUB segmented-sort path.
+// free) -- that is the reference's insertion order.  The cell is then stored
+// grouped by z quarter (volume.cuh): z bins computed coalesced, a lane per
+// cell turns them into stable destinations + the bins word, and the records
+// are written back coalesced with perm.  Runs longer than kSmallRun are listed
+// for the CUB segmented-sort path; they, and the small runs of a warp that
+// has one, stay in insertion order (bins 0, perm 0).
 template <class Rec>
 __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
                                                           const uint32_t* __restrict__ offsets,
                                                           const unsigned long long* __restrict__ keys,
                                                           uint32_t ncells, uint4* records,
-                                                          uint32_t* big_cells, uint32_t* n_big) {
+                                                          uint32_t* big_cells, uint32_t* n_big,
+                                                          BinOut bo) {
   __shared__ SealSmem smem[kSealWarps];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   SealSmem& sm = smem[warp];
@@ -260,9 +284,28 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       sm.st[j * kPitch + lane] = x;
     }
     __syncwarp();
+    for (uint32_t i = lane; i < len; i += 32) {  // z bin of every sealed sample
+      const uint32_t col = sm.cell_of[i];
+      const float z = rec.z_of(sm.st[(i - sm.cstart[col]) * kPitch + col]);
+      const int64_t iz = (int64_t)(c0 + col) % bo.nz;
+      sm.slot[i] = (uint8_t)((z >= zbin_bound(bo.oz, bo.voxel, iz, 1)) + (z >= zbin_bound(bo.oz, bo.voxel, iz, 2)) +
+                             (z >= zbin_bound(bo.oz, bo.voxel, iz, 3)));
+    }
+    __syncwarp();
+    if (c < ncells) {  // lane = cell: stable destinations by bin, bins word
+      const uint32_t r0 = cs - s0;
+      uint32_t n[4] = {0, 0, 0, 0};
+      for (uint32_t j = 0; j < cn; ++j) ++n[sm.slot[r0 + j]];
+      uint32_t next[4] = {0, n[0], n[0] + n[1], n[0] + n[1] + n[2]};
+      for (uint32_t j = 0; j < cn; ++j) sm.slot[r0 + j] = (uint8_t)(next[sm.slot[r0 + j]]++);
+      bo.bins[c] = n[0] | ((n[0] + n[1]) << 8) | ((n[0] + n[1] + n[2]) << 16) | (1u << 24);
+    }
+    __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t col = sm.cell_of[i];
-      records[s0 + i] = rec(sm.st[(i - sm.cstart[col]) * kPitch + col]);
+      const uint32_t j = i - sm.cstart[col], dest = sm.slot[i];
+      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col]);
+      bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
   } else if (cn > 0 && !big) {
     // a big run in this warp's chunk: the small runs are sealed lane by lane
@@ -276,7 +319,15 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       }
       k[j] = x;
     }
-    for (uint32_t i = 0; i < cn; ++i) records[cs + i] = rec(k[i]);
+    for (uint32_t i = 0; i < cn; ++i) {
+      records[cs + i] = rec(k[i]);
+      bo.perm[cs + i] = 0;
+    }
+  }
+  if (!staged && c < ncells) {  // insertion order kept (big runs: sorted by the CUB path)
+    bo.bins[c] = 0;
+    if (big)
+      for (uint32_t i = 0; i < cn; ++i) bo.perm[cs + i] = 0;
   }
 }
 
@@ -331,7 +382,12 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   vol->n_samples = n_kept;
   vol->rejected = (int64_t)n_rej;
   dev_alloc(&vol->d_records, sizeof(uint4) * std::max<uint32_t>(n_kept, 1));
-  if (n_kept == 0) return;
+  dev_alloc(&vol->d_perm, std::max<uint32_t>(n_kept, 1));
+  dev_alloc(&vol->d_bins, sizeof(uint32_t) * std::max<int64_t>(ncells, 1));
+  if (n_kept == 0) {
+    DARE_CUDA(cudaMemsetAsync(vol->d_bins, 0, sizeof(uint32_t) * std::max<int64_t>(ncells, 1), s));
+    return;
+  }
   Scratch<unsigned long long> keys(n_kept, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncells, s));
   pt.mark("readback+alloc");
@@ -343,7 +399,8 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s) {
   Scratch<uint32_t> n_big_d(1, s);
   DARE_CUDA(cudaMemsetAsync(n_big_d.ptr, 0, sizeof(uint32_t), s));
   seal_k<<<ceil_div(ncells, 32 * kSealWarps), 32 * kSealWarps, 0, s>>>(
-      rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr);
+      rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr,
+      BinOut{vol->origin[2], vol->voxel, vol->dims[2], vol->d_bins, vol->d_perm});
   DARE_CUDA(cudaGetLastError());
   pt.mark("seal");
   uint32_t n_big = 0;
@@ -434,7 +491,6 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
         frame_scatter_k<false><<<grid, 256, 0, s>>>(fv, m, counts, offsets, keys, rej);
     };
     build_csr(vol.get(), FrameRecords{fv}, scatter, s);
-    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
     *out = vol.release();
@@ -483,7 +539,6 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
                                                                          offsets, keys, rej);
     };
     build_csr(vol.get(), SampleRecords{d_pos.ptr, d_word.ptr}, scatter, s);
-    bin_volume(vol.get(), s);
     DARE_CUDA(cudaStreamSynchronize(s));
     *out = vol.release();
   });
