@@ -5,11 +5,12 @@
 // volume.py:240-269 (seal: stable argsort by linear cell + bincount + cumsum).
 //
 // Device pipeline (all FP64 chains bit-identical to numpy; -fmad=false):
-//   1. count : per pixel -> cell; warp-aggregated u32 histogram
-//              (__match_any_sync groups equal cells, one atomic per group);
-//              out-of-bounds pixels counted (volume.py:230-233).
+//   1. count : per pixel -> cell; runs of consecutive frames in one cell are
+//              aggregated per thread, flushes warp-aggregated (__match_any_sync
+//              groups equal cells, one atomic per group); out-of-bounds pixels
+//              counted (volume.py:230-233).
 //   2. scan  : exclusive prefix of counts -> cell offsets (CUB).
-//   3. fill  : per pixel -> slot = offset + atomic cursor; stores the 64-bit
+//   3. fill  : same runs -> slots = offset + atomic cursor; stores the 64-bit
 //              key (insertion index << 8 | intensity); the insertion index is
 //              synchronized frame * H*W + row-major pixel.
 //   4. seal  : per cell, sort its (tiny) key run ascending = insertion order --
@@ -61,24 +62,6 @@ struct FrameView {
   FastDiv div_w, div_hw;
 };
 
-// Pixel (u, v) of a frame with axes fa = {c0[3], c1[3], t[3]}: f32 world
-// position (reconstruct.py:156-162) and linear cell, or -1 when out of bounds.
-__device__ __forceinline__ int32_t pixel_cell32(const double* __restrict__ fa, uint32_t u,
-                                                uint32_t v, double px, double py,
-                                                const VoxelMap& m) {
-  const double U = (double)u * px, V = (double)v * py;
-  bool ok = true;
-  uint32_t idx[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const float p32 = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
-    const double f = floor(voxel_coord(m, a, p32));
-    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
-    idx[a] = ok ? (uint32_t)f : 0u;
-  }
-  return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
-}
-
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // Warp-aggregated histogram (kFill=false) or slot assignment (kFill=true):
@@ -105,46 +88,114 @@ __device__ __forceinline__ void warp_scatter(bool kept, int32_t lin, unsigned lo
   }
 }
 
-// Frames: a block covers a 16(u) x 4(v) x 4(frames) brick of pixels and each
-// warp an 8 x 2 x 2 sub-brick, so that pixels landing in the same cell --
-// neighbours in the image and in consecutive frames of a sweep -- meet in one
-// warp and share one atomic.  (Slot order inside a cell is irrelevant: seal
-// sorts every run by insertion key.)  grid: x = (u,v) tiles, y = frame groups.
-constexpr int kBrickU = 16, kBrickV = 4, kBrickF = 4;
+// Frames.  Thread = one pixel (u, v) over a chunk of kRunFrames consecutive
+// synchronized frames; warp = an 8(u) x 4(v) patch, block = 16 x 16 pixels.
+// Consecutive frames of a sweep put a pixel into the same cell for several
+// frames, so each thread keeps a run (cell, first frame, length <= kMaxRun,
+// the run's intensities) and only flushes when the cell changes; a flush is
+// warp-aggregated over lanes flushing the same cell (image neighbours): one
+// atomic per group, ranks inside the group from a bit-sliced ballot prefix of
+// the run lengths.  Count pass: u32 histogram; fill pass: slot = cell offset +
+// returned cursor + rank, keys written for every sample of the run.  (Slot
+// order inside a cell is irrelevant: seal sorts every run by insertion key.)
+constexpr int kRunFrames = 64;
+constexpr int kMaxRun = 8;  // intensities buffered in two u32
+
+template <bool kInv>
+__device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, double V, const VoxelMap& m) {
+  bool ok = true;
+  uint32_t idx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double d = (double)__double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]) - m.origin[a];
+    const double f = floor(kInv ? d * m.inv_voxel : d / m.voxel);
+    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
+    idx[a] = ok ? (uint32_t)f : 0u;
+  }
+  return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
+}
 
 template <bool kFill>
-__global__ void __launch_bounds__(256) frame_scatter_k(FrameView fv, VoxelMap m,
-                                                       uint32_t* counts,
-                                                       const uint32_t* __restrict__ offsets,
-                                                       unsigned long long* keys,
-                                                       unsigned long long* rejected) {
-  // No block barriers: each warp strides over its frames independently, so the
-  // latency of one frame's (returning) atomics overlaps other warps' work.
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const uint32_t tiles_u = (fv.W + kBrickU - 1) / kBrickU;
-  const uint32_t tu = blockIdx.x % tiles_u, tv = blockIdx.x / tiles_u;
-  const uint32_t u = tu * kBrickU + (warp & 1) * 8 + (lane & 7);
-  const uint32_t v = tv * kBrickV + ((warp >> 1) & 1) * 2 + ((lane >> 3) & 1);
-  const uint32_t fl = (warp >> 2) * 2 + (lane >> 4);  // frame within the brick
+__device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, uint32_t run_f,
+                                          uint32_t ib0, uint32_t ib1, uint32_t p, uint32_t hw,
+                                          uint32_t* counts, const uint32_t* __restrict__ offsets,
+                                          unsigned long long* keys) {
+  const unsigned lane = lane_id();
+  // lanes not flushing get a key no cell has, so MATCH runs on the full warp
+  const unsigned peers = __match_any_sync(0xffffffffu, need ? (unsigned)lin : (0x80000000u | lane));
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned total = 0, prefix = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {  // k <= kMaxRun < 16
+    const unsigned mb = __ballot_sync(0xffffffffu, need && ((k >> b) & 1u)) & peers;
+    total += (unsigned)__popc(mb) << b;
+    prefix += (unsigned)__popc(mb & lt) << b;
+  }
+  const unsigned leader = __ffs(peers) - 1;
+  if (!kFill) {
+    if (need && lane == leader) atomicAdd(&counts[lin], total);
+  } else {
+    unsigned base = 0;
+    if (need && lane == leader) base = atomicAdd(&counts[lin], total);
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (need) {
+      unsigned long long* dst = keys + offsets[lin] + base + prefix;
+      for (uint32_t t = 0; t < k; ++t) {
+        const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
+        dst[t] = ((unsigned long long)((run_f + t) * hw + p) << 8) | inten;
+      }
+    }
+  }
+}
+
+template <bool kFill, bool kInv>
+__global__ void __launch_bounds__(256) frame_run_k(FrameView fv, VoxelMap m, uint32_t* counts,
+                                                   const uint32_t* __restrict__ offsets,
+                                                   unsigned long long* keys,
+                                                   unsigned long long* rejected) {
+  __shared__ double s_axes[kRunFrames * 9];
+  __shared__ uint32_t s_img[kRunFrames];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t tiles_u = (fv.W + 15) / 16;
+  const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
   const uint32_t p = v * fv.W + u;
   const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
-  const double* __restrict__ axes = fv.axes;
-  for (uint32_t f0 = blockIdx.y * kBrickF; f0 < fv.n_frames; f0 += gridDim.y * kBrickF) {
-    const uint32_t f = f0 + fl;
-    const bool valid = in_frame && f < fv.n_frames;
-    const int32_t lin = valid ? pixel_cell32(axes + (size_t)f * 9, u, v, fv.px, fv.py, m) : -1;
-    const bool kept = lin >= 0;
+  const uint32_t f0 = blockIdx.y * kRunFrames;
+  const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[(size_t)f0 * 9 + i];
+  if (kFill)
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (uint32_t)fv.image[f0 + i];
+  __syncthreads();
+  const double U = (double)u * fv.px, V = (double)v * fv.py;
+  int32_t cur = -1;
+  uint32_t run_f = 0, k = 0, ib0 = 0, ib1 = 0;
+  for (int j = 0; j < nf; ++j) {  // block-uniform trip count
+    const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m) : -1;
     if (!kFill) {
-      const unsigned oob = __ballot_sync(0xffffffffu, valid && !kept);
+      const unsigned oob = __ballot_sync(0xffffffffu, in_frame && lin < 0);
       if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
     }
-    unsigned long long key = 0;
-    if (kFill && kept) {
-      const uint32_t inten = fv.frames[(size_t)fv.image[f] * fv.hw + p];
-      key = ((unsigned long long)(f * fv.hw + p) << 8) | inten;
+    const bool restart = lin != cur || k == (uint32_t)kMaxRun;
+    const bool need = restart && cur >= 0;
+    if (__any_sync(0xffffffffu, need))
+      run_flush<kFill>(need, cur, k, run_f, ib0, ib1, p, fv.hw, counts, offsets, keys);
+    if (restart) {
+      cur = lin;
+      run_f = f0 + j;
+      k = 0;
+      ib0 = ib1 = 0;
     }
-    warp_scatter<kFill>(kept, lin, key, counts, offsets, keys);
+    if (kFill && lin >= 0) {
+      const uint32_t inten = fv.frames[(size_t)s_img[j] * fv.hw + p];
+      if (k < 4) ib0 |= inten << (8 * k);
+      else ib1 |= inten << (8 * (k - 4));
+    }
+    ++k;
   }
+  const bool need = cur >= 0;
+  if (__any_sync(0xffffffffu, need))
+    run_flush<kFill>(need, cur, k, run_f, ib0, ib1, p, fv.hw, counts, offsets, keys);
 }
 
 // Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index.
@@ -478,17 +529,18 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
       DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
                                 cudaMemcpyHostToDevice, s));
     }
-    // a block keeps its (u, v) brick and strides over frame groups, so the
-    // per-thread setup is amortised over many frames
-    dim3 grid(ceil_div(width, kBrickU) * ceil_div(height, kBrickV),
-              (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n_frames, kBrickF), 1), 8));
+    DARE_LIMIT(ceil_div(n_frames, kRunFrames) <= 65535, "too many frames for one launch");
+    const dim3 grid(ceil_div(width, 16) * ceil_div(height, 16),
+                    (unsigned)std::max<int64_t>(ceil_div(n_frames, kRunFrames), 1));
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
                        unsigned long long* keys, unsigned long long* rej) {
       if (n_frames == 0) return;
       if (fill)
-        frame_scatter_k<true><<<grid, 256, 0, s>>>(fv, m, counts, offsets, keys, rej);
+        (m.exact_inv ? frame_run_k<true, true> : frame_run_k<true, false>)<<<grid, 256, 0, s>>>(
+            fv, m, counts, offsets, keys, rej);
       else
-        frame_scatter_k<false><<<grid, 256, 0, s>>>(fv, m, counts, offsets, keys, rej);
+        (m.exact_inv ? frame_run_k<false, true> : frame_run_k<false, false>)<<<grid, 256, 0, s>>>(
+            fv, m, counts, offsets, keys, rej);
     };
     build_csr(vol.get(), FrameRecords{fv}, scatter, s);
     DARE_CUDA(cudaStreamSynchronize(s));
