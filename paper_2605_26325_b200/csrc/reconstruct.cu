@@ -273,6 +273,7 @@ struct SealSmem {
   uint16_t cstart[32];                         // cell start relative to the warp's first key
   uint8_t cell_of[kSmallRun * 32];             // key position -> lane of its cell (0xff: big run)
   uint8_t slot[kSmallRun * 32];                // key position -> z bin, then destination in its cell
+  float zb[3][32];                             // z-quarter boundaries of each lane's cell
 };
 
 // z-quarter binning of the sealed runs (layout in volume.cuh)
@@ -334,13 +335,16 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       }
       sm.st[j * kPitch + lane] = x;
     }
+    {
+      const int64_t iz = (int64_t)c % bo.nz;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) sm.zb[q][lane] = zbin_bound(bo.oz, bo.voxel, iz, q + 1);
+    }
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {  // z bin of every sealed sample
       const uint32_t col = sm.cell_of[i];
       const float z = rec.z_of(sm.st[(i - sm.cstart[col]) * kPitch + col]);
-      const int64_t iz = (int64_t)(c0 + col) % bo.nz;
-      sm.slot[i] = (uint8_t)((z >= zbin_bound(bo.oz, bo.voxel, iz, 1)) + (z >= zbin_bound(bo.oz, bo.voxel, iz, 2)) +
-                             (z >= zbin_bound(bo.oz, bo.voxel, iz, 3)));
+      sm.slot[i] = (uint8_t)((z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]));
     }
     __syncwarp();
     if (c < ncells) {  // lane = cell: stable destinations by bin, bins word
