@@ -563,8 +563,9 @@ def run_b200(args):
     if args.exact:
         main_kernel = f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>"
     else:
-        smem_gate = schedule == 1 and int(info.n_orientations) <= 1024
-        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {1 if smem_gate else 0}>"
+        n_or = int(info.n_orientations)
+        gmode = 2 if n_or == 1 else (1 if schedule == 1 and n_or <= 1024 else 0)  # register / smem / global gate
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}>"
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
     # [fallback kernel on the certified path]

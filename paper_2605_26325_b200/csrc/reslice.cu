@@ -170,7 +170,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 
 constexpr int kSmemBytes = 4096;                        // gate table staged in shared memory
-constexpr int kGateSmem = kSmemBytes / sizeof(double);  // exact path (f64 entries)
+constexpr int kGateSmemD = kSmemBytes / sizeof(double);  // exact path (f64 entries)
 constexpr int kGateSmemF = kSmemBytes / sizeof(float);  // certified path (f32 entries)
 
 // Launch mapping.  Pixel-major: 256 threads = one 16x16 pixel tile of one pose
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
   bool active;
   map_pixel(a, pose, u, v, active);
   bool gate_filter;
-  const double* gate = stage_gate<double, kGateSmem>(a, a.gate + (size_t)pose * a.n_orient,
+  const double* gate = stage_gate<double, kGateSmemD>(a, a.gate + (size_t)pose * a.n_orient,
                                                      reinterpret_cast<double*>(smem_raw), gate_filter);
   Walk w;
   w.init(a, pose, u, v, active);
@@ -450,11 +450,18 @@ struct FastWalk {
 
 // One visited record on the certified path: exact survivor test, f32 weight
 // 2^(A2 - dist * c2) (0 for non-survivors), accumulated into the batch sums.
-template <int kDistMode, bool kSmemGate>
+// Gate sources: kGateGlobal (pose-major launches / large tables), kGateSmem
+// (pixel-major: the pose's row staged in shared memory), kGateSingle (volume
+// with one orientation id, e.g. linear sweeps with a fixed probe: the pose's
+// single gate value lives in a register and no lookup is made).
+constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2;
+
+template <int kDistMode, int kGate>
 __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
-                                          const float* gate, const float (&wh)[3],
+                                          const float* gate, float g_single, const float (&wh)[3],
                                           const float (&wl)[3], float c2, float& bw, float& bj) {
-  const float g = kSmemGate ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8));
+  const float g = kGate == kGateSingle ? g_single
+                                       : (kGate == kGateSmem ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8)));
   const bool k = valid && w.in_cube(c) && g != CUDART_INF_F;
   float arg = g;
   if (kDistMode != 2) {
@@ -517,7 +524,7 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 
 // Certified path: same mapping as reslice_k; branch-free f32 weights for
 // every visited record (no warp rounds), 4 loads in flight, phased walk.
-template <int kDistMode, bool kSmemGate>
+template <int kDistMode, int kGate>
 __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                       uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -525,7 +532,8 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
   bool active;
   map_pixel(a, pose, u, v, active);
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
-  if (kSmemGate) {  // pixel-major launch: one pose per block
+  const float g_single = kGate == kGateSingle ? __ldg(gate) : 0.0f;
+  if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
     float* sg = reinterpret_cast<float*>(smem_raw);
     for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) sg[i] = gate[i];
     __syncthreads();
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     float bw = 0.0f, bj = 0.0f;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      fast_term<kDistMode, kSmemGate>(r[i], i0 + i >= w.s && i0 + i < w.e, w, gate, wh, wl, c2, bw, bj);
+      fast_term<kDistMode, kGate>(r[i], i0 + i >= w.s && i0 + i < w.e, w, gate, g_single, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
     i0 += 4;
@@ -828,10 +836,12 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_k<0>);
     set_smem(reslice_k<1>);
     set_smem(reslice_k<2>);
-    set_smem(reslice_fast_k<0, true>);
-    set_smem(reslice_fast_k<0, false>);
-    set_smem(reslice_fast_k<2, true>);
-    set_smem(reslice_fast_k<2, false>);
+    set_smem(reslice_fast_k<0, kGateGlobal>);
+    set_smem(reslice_fast_k<0, kGateSmem>);
+    set_smem(reslice_fast_k<0, kGateSingle>);
+    set_smem(reslice_fast_k<2, kGateGlobal>);
+    set_smem(reslice_fast_k<2, kGateSmem>);
+    set_smem(reslice_fast_k<2, kGateSingle>);
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -852,11 +862,14 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.amb = amb.ptr;
   a.amb_count = amb_count.ptr;
   DARE_CUDA(cudaMemsetAsync(amb_count.ptr, 0, sizeof(unsigned), s));
-  const bool smem_gate = !a.pose_major && a.n_orient <= kGateSmemF;
-  if (a.dist_mode == 2)
-    (smem_gate ? reslice_fast_k<2, true> : reslice_fast_k<2, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
-  else
-    (smem_gate ? reslice_fast_k<0, true> : reslice_fast_k<0, false>)<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  const int gmode = a.n_orient == 1 ? kGateSingle
+                                    : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal);
+  auto k = a.dist_mode == 2
+               ? (gmode == kGateSingle ? reslice_fast_k<2, kGateSingle>
+                                       : (gmode == kGateSmem ? reslice_fast_k<2, kGateSmem> : reslice_fast_k<2, kGateGlobal>))
+               : (gmode == kGateSingle ? reslice_fast_k<0, kGateSingle>
+                                       : (gmode == kGateSmem ? reslice_fast_k<0, kGateSmem> : reslice_fast_k<0, kGateGlobal>));
+  k<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");
   DARE_CUDA(cudaGetLastError());
   const unsigned fb_grid = (unsigned)sm_count() * 2;
