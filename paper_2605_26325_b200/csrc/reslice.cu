@@ -465,10 +465,13 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
   const bool k = valid && w.in_cube(c) && g != CUDART_INF_F;
   float arg = g;
   if (kDistMode != 2) {
-    const float dx = __fsub_rn(__fsub_rn(__uint_as_float(c.x), wh[0]), wl[0]);
-    const float dy = __fsub_rn(__fsub_rn(__uint_as_float(c.y), wh[1]), wl[1]);
+    // (x, y) as one f32x2 lane pair (FADD2 / FMUL2); same roundings as scalar
+    const float2 dxy = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(c.x), __uint_as_float(c.y)),
+                                             make_float2(-wh[0], -wh[1])),
+                                  make_float2(-wl[0], -wl[1]));
     const float dz = __fsub_rn(__fsub_rn(__uint_as_float(c.z), wh[2]), wl[2]);
-    const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    const float2 sq = __fmul2_rn(dxy, dxy);
+    const float d2 = __fmaf_rn(dz, dz, __fadd_rn(sq.x, sq.y));
     const float dist = sqrt_approx(d2);  // subnormal d2 flushes: |error| < 1.1e-19 (abs slack)
     arg = __fmaf_rn(-dist, c2, g);
   }
