@@ -433,3 +433,30 @@ def test_z_binned_layout_round_trips_every_run_length():
     ref = oracle.reslice(v, oracle.plane_params(plane), oracle.cfg_array(cfg), 40, 1, 0)
     np.testing.assert_array_equal(got.pixels, ref[0])
     np.testing.assert_array_equal(got.coverage, ref[1])
+
+
+def test_certified_path_guard_rails(rng):
+    """Extreme weighting configs: exponents beyond the accurate ex2 range make
+    the certified path stand down for the launch (exact FP64 everywhere), tiny
+    radii / huge k_dist put many pixels near the coverage threshold; both must
+    still match the FP64 path and the oracle bit for bit."""
+    vol = _random_volume(rng, 20000, 10.0, 0.5)
+    planes = []
+    for _ in range(6):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        planes.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(2, 8, 3)), 19, 17, (0.3, 0.3)))
+    cfgs = [ResliceConfig(interp_radius=0.4, k_normal=1000.0, k_inplane=1000.0, k_dist=50.0,
+                          normal_threshold_deg=89.0, inplane_threshold_deg=89.0),   # M > 99: exact path
+            ResliceConfig(interp_radius=0.4, k_dist=16.0, normal_threshold_deg=85.0,
+                          inplane_threshold_deg=85.0, k_normal=0.0, k_inplane=0.0),  # weights down to e^-27.7
+            ResliceConfig(interp_radius=0.05, k_dist=0.0)]
+    for cfg in cfgs:
+        fa = _reslice_raw(vol, planes, cfg, False)
+        ex = _reslice_raw(vol, planes, cfg, True)
+        np.testing.assert_array_equal(fa[0], ex[0])
+        np.testing.assert_array_equal(fa[1], ex[1])
+        ref = oracle.reslice(vol, oracle.plane_params(planes[0]), oracle.cfg_array(cfg), 19, 17,
+                             cfg.unassigned_value)
+        np.testing.assert_array_equal(fa[0][0], ref[0])
+        np.testing.assert_array_equal(fa[1][0].astype(bool), ref[1])
