@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, VoxelMap m, uin
     run_flush<kFill>(need, cur, k, run_f, ib0, ib1, p, fv.hw, counts, offsets, keys);
 }
 
-// Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index.
+// Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index << 8.
 template <bool kFill>
 __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict__ pos, int64_t n,
                                                         VoxelMap m, uint32_t* counts,
@@ -224,13 +224,12 @@ __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict_
     const int oob = __syncthreads_count(valid && !kept);
     if (threadIdx.x == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
   }
-  warp_scatter<kFill>(kept, lin, (unsigned long long)i, counts, offsets, keys);
+  warp_scatter<kFill>(kept, lin, (unsigned long long)i << 8, counts, offsets, keys);
 }
 
 struct FrameRecords {
   FrameView fv;
-  __device__ __forceinline__ uint4 operator()(unsigned long long key) const {
-    const uint32_t pid = (uint32_t)(key >> 8);
+  __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t inten) const {
     const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
     const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
     const double* fa = fv.axes + (size_t)f * 9;
@@ -240,11 +239,10 @@ struct FrameRecords {
     for (int a = 0; a < 3; ++a)
       p32[a] = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
     return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
-                      (fv.oid[f] << 8) | (uint32_t)(key & 0xffu));
+                      (fv.oid[f] << 8) | inten);
   }
   // z only (the binning key), same arithmetic as operator()
-  __device__ __forceinline__ float z_of(unsigned long long key) const {
-    const uint32_t pid = (uint32_t)(key >> 8);
+  __device__ __forceinline__ float z_of(uint32_t pid) const {
     const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
     const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
     const double* fa = fv.axes + (size_t)f * 9;
@@ -256,20 +254,21 @@ struct FrameRecords {
 struct SampleRecords {
   const float* pos;
   const uint32_t* word;  // (oid << 8) | intensity
-  __device__ __forceinline__ uint4 operator()(unsigned long long key) const {
-    const size_t i = (size_t)key;
+  __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t) const {
+    const size_t i = (size_t)pid;
     return make_uint4(__float_as_uint(pos[3 * i]), __float_as_uint(pos[3 * i + 1]),
                       __float_as_uint(pos[3 * i + 2]), word[i]);
   }
-  __device__ __forceinline__ float z_of(unsigned long long key) const { return pos[3 * (size_t)key + 2]; }
+  __device__ __forceinline__ float z_of(uint32_t pid) const { return pos[3 * (size_t)pid + 2]; }
 };
 
 constexpr int kSmallRun = 32;  // per-cell runs sorted in shared memory by one lane
 constexpr int kSealWarps = 4;  // warps per seal block
-constexpr int kPitch = 33;     // odd row pitch (in u64): both access patterns conflict-free
+constexpr int kPitch = 33;     // odd row pitch: both access patterns conflict-free
 
 struct SealSmem {
-  unsigned long long st[kSmallRun * kPitch];  // st[k * kPitch + lane] = k-th key of cell c0+lane
+  uint32_t st[kSmallRun * kPitch];             // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
+  uint8_t si[kSmallRun * kPitch];              // its low key byte (intensity for frames)
   uint16_t cstart[32];                         // cell start relative to the warp's first key
   uint8_t cell_of[kSmallRun * 32];             // key position -> lane of its cell (0xff: big run)
   uint8_t slot[kSmallRun * 32];                // key position -> z bin, then destination in its cell
@@ -323,17 +322,24 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t col = sm.cell_of[i];
-      sm.st[(i - sm.cstart[col]) * kPitch + col] = keys[s0 + i];
+      // key = insertion index << 8 | byte: staged as u32 + u8 (smaller stage, more warps)
+      const unsigned long long key = keys[s0 + i];
+      const uint32_t at = (i - sm.cstart[col]) * kPitch + col;
+      sm.st[at] = (uint32_t)(key >> 8);
+      sm.si[at] = (uint8_t)key;
     }
     __syncwarp();
-    for (uint32_t i = 1; i < cn; ++i) {
-      const unsigned long long x = sm.st[i * kPitch + lane];
+    for (uint32_t i = 1; i < cn; ++i) {  // by insertion index; the byte moves along
+      const uint32_t x = sm.st[i * kPitch + lane];
+      const uint8_t xi = sm.si[i * kPitch + lane];
       uint32_t j = i;
       while (j > 0 && sm.st[(j - 1) * kPitch + lane] > x) {
         sm.st[j * kPitch + lane] = sm.st[(j - 1) * kPitch + lane];
+        sm.si[j * kPitch + lane] = sm.si[(j - 1) * kPitch + lane];
         --j;
       }
       sm.st[j * kPitch + lane] = x;
+      sm.si[j * kPitch + lane] = xi;
     }
     {
       const int64_t iz = (int64_t)c % bo.nz;
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {  // z bin of every sealed sample
       const uint32_t col = sm.cell_of[i];
-      const float z = rec.z_of(sm.st[(i - sm.cstart[col]) * kPitch + col]);
+      const float z = rec.z_of(sm.st[(i - sm.cstart[col]) * kPitch + col]);  // insertion index
       sm.slot[i] = (uint8_t)((z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]));
     }
     __syncwarp();
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t col = sm.cell_of[i];
       const uint32_t j = i - sm.cstart[col], dest = sm.slot[i];
-      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col]);
+      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col], sm.si[j * kPitch + col]);
       bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
   } else if (cn > 0 && !big) {
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       k[j] = x;
     }
     for (uint32_t i = 0; i < cn; ++i) {
-      records[cs + i] = rec(k[i]);
+      records[cs + i] = rec((uint32_t)(k[i] >> 8), (uint32_t)(k[i] & 0xffu));
       bo.perm[cs + i] = 0;
     }
   }
@@ -401,7 +407,8 @@ template <class Rec>
 __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_t* ends,
                                   const unsigned long long* __restrict__ sorted, uint4* records) {
   uint32_t b = begins[blockIdx.x], e = ends[blockIdx.x];
-  for (uint32_t s = b + threadIdx.x; s < e; s += blockDim.x) records[s] = rec(sorted[s]);
+  for (uint32_t s = b + threadIdx.x; s < e; s += blockDim.x)
+    records[s] = rec((uint32_t)(sorted[s] >> 8), (uint32_t)(sorted[s] & 0xffu));
 }
 
 // count -> scan -> fill -> seal, shared by frames and arbitrary samples.
