@@ -227,27 +227,54 @@ __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict_
   warp_scatter<kFill>(kept, lin, (unsigned long long)i << 8, counts, offsets, keys);
 }
 
+// Seal-side frame table (80 B per frame): per axis a the pair (R[a][0],
+// R[a][1]) as one 16 B load plus t[a], and the orientation id -- 7 loads per
+// record instead of 10 (the seal is bound by L1 wavefronts on these lookups).
+struct SealAxes {
+  double2 r[3];
+  double t[3];
+  uint32_t oid, pad;
+};
+
+__global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __restrict__ oid,
+                            uint32_t n, SealAxes* out) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  const double* fa = axes + (size_t)f * 9;
+  SealAxes x;
+  for (int a = 0; a < 3; ++a) {
+    x.r[a] = make_double2(fa[a], fa[3 + a]);
+    x.t[a] = fa[6 + a];
+  }
+  x.oid = oid[f];
+  x.pad = 0;
+  out[f] = x;
+}
+
 struct FrameRecords {
   FrameView fv;
+  const SealAxes* sa;
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t inten) const {
     const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
     const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
-    const double* fa = fv.axes + (size_t)f * 9;
+    const SealAxes& x = sa[f];
     const double U = (double)u * fv.px, V = (double)v * fv.py;
     float p32[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      p32[a] = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
+    for (int a = 0; a < 3; ++a) {  // reconstruct.py:156-162: ((U*R[a,0]) + (V*R[a,1])) + t[a]
+      const double2 r = x.r[a];
+      p32[a] = __double2float_rn((U * r.x + V * r.y) + x.t[a]);
+    }
     return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
-                      (fv.oid[f] << 8) | inten);
+                      (x.oid << 8) | inten);
   }
   // z only (the binning key), same arithmetic as operator()
   __device__ __forceinline__ float z_of(uint32_t pid) const {
     const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
     const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
-    const double* fa = fv.axes + (size_t)f * 9;
+    const double2 r = sa[f].r[2];
     const double U = (double)u * fv.px, V = (double)v * fv.py;
-    return __double2float_rn((U * fa[2] + V * fa[5]) + fa[8]);
+    return __double2float_rn((U * r.x + V * r.y) + sa[f].t[2]);
   }
 };
 
@@ -562,8 +589,14 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
         (m.exact_inv ? frame_run_k<false, true> : frame_run_k<false, false>)<<<grid, 256, 0, s>>>(
             fv, m, counts, offsets, keys, rej);
     };
+    Scratch<SealAxes> sa((size_t)std::max<int64_t>(n_frames, 1), s);
+    if (n_frames > 0) {
+      seal_axes_k<<<ceil_div(n_frames, 256), 256, 0, s>>>(fs.d_axes, d_oid.ptr, (uint32_t)n_frames, sa.ptr);
+      DARE_CUDA(cudaGetLastError());
+    }
     // measured: cfg3 (8000 frames, 576 KB of axes) seal 52.3 -> 46.0 ms at 75%
-    build_csr(vol.get(), FrameRecords{fv}, scatter, s, n_frames * 72 > (128 << 10) ? 75 : -1);
+    build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s,
+              n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1);
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
     *out = vol.release();
