@@ -133,10 +133,18 @@ def rotate_many(quats: np.ndarray, vecs: np.ndarray) -> np.ndarray:
         raise InvalidArgumentError(
             f"quaternion norm {float(norms[bad][0]):.6f} deviates from 1 by more than {UNIT_NORM_TOL}"
         )
-    u = quats[:, 1:4]
-    v = np.broadcast_to(np.asarray(vecs, dtype=float), u.shape)
-    t = 2.0 * np.cross(u, v)
-    return v + quats[:, 0:1] * t + np.cross(u, t)
+    # np.cross restated per component with numpy's own order (a1*b2 - a2*b1,
+    # a2*b0 - a0*b2, a0*b1 - a1*b0; separately rounded): identical bits,
+    # without np.cross's per-call axis shuffling
+    w, u0, u1, u2 = quats[:, 0], quats[:, 1], quats[:, 2], quats[:, 3]
+    v = np.broadcast_to(np.asarray(vecs, dtype=float), (len(quats), 3))
+    v0, v1, v2 = v[:, 0], v[:, 1], v[:, 2]
+    t0, t1, t2 = 2.0 * (u1 * v2 - u2 * v1), 2.0 * (u2 * v0 - u0 * v2), 2.0 * (u0 * v1 - u1 * v0)
+    out = np.empty((len(quats), 3))
+    out[:, 0] = (v0 + w * t0) + (u1 * t2 - u2 * t1)
+    out[:, 1] = (v1 + w * t1) + (u2 * t0 - u0 * t2)
+    out[:, 2] = (v2 + w * t2) + (u0 * t1 - u1 * t0)
+    return out
 
 
 def rotation_matrices(quats: np.ndarray) -> np.ndarray:
