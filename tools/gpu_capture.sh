@@ -11,6 +11,6 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none \
   --csv --log-file gpurun_out/launches_cfg2.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "launches=$?" >> gpurun_out/status.txt
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"reslice_fast_k" -s 2 -c 1 \
   -o gpurun_out/full_reslice $CMD > gpurun_out/ncu_full_reslice.log 2>&1; echo "full_reslice=$?" >> gpurun_out/status.txt
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"frame_scatter_k|seal_k|bin_cells_k|compound_k" -s 4 -c 4 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"frame_run_k|seal_k|bin_cells_k|compound_k" -s 4 -c 4 \
   -o gpurun_out/full_recon $CMD > gpurun_out/ncu_full_recon.log 2>&1; echo "full_recon=$?" >> gpurun_out/status.txt
 cat gpurun_out/status.txt
