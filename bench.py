@@ -565,7 +565,7 @@ def run_b200(args):
     else:
         n_or = int(info.n_orientations)
         gmode = 2 if n_or == 1 else (1 if schedule == 1 and n_or <= 1024 else 0)  # register / smem / global gate
-        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}>"
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}, false>"
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
     # [fallback kernel on the certified path]

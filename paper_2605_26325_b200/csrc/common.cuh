@@ -79,6 +79,24 @@ struct Scratch {
 
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
+// Grow-only device buffer per (host thread, device, slot), for scratch of work
+// enqueued on the thread's own stream: stream order makes reuse across calls
+// safe and saves the per-call allocator round trips of small launches.
+void* thread_arena(int slot, size_t bytes, cudaStream_t s);
+
+// Bump carving of one scratch block (256 B aligned pieces).
+struct Carve {
+  uint8_t* base = nullptr;
+  size_t off = 0;
+  static size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
+  template <class T>
+  T* take(size_t n) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += up(n * sizeof(T));
+    return p;
+  }
+};
+
 // Development aid: with DARE_PROFILE=1 in the environment, records CUDA events
 // at phase boundaries on `stream` and prints per-phase device times to stderr
 // when it goes out of scope.  No cost when disabled.

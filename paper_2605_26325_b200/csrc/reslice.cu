@@ -33,6 +33,7 @@
 #include <math_constants.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "dare_exp.h"
 #include <cub/device/device_radix_sort.cuh>
@@ -52,6 +53,8 @@ constexpr double kEps64 = 1.1102230246251565e-16;   // 2^-53
 constexpr double kEx2Err = 4.76837158203125e-07;    // 2^-21
 constexpr double kSqrtErr = 4.76837158203125e-07;   // 2^-21
 constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fast path accepts
+constexpr int kSplitMaxPoses = 4;      // pixel-major batches up to this size split pixels over 4 threads
+constexpr size_t kArenaMax = 256ull << 20;  // larger scratch uses stream-ordered allocations
 
 struct ResliceArgs {
   const uint32_t* offsets;
@@ -410,7 +413,9 @@ struct FastWalk {
   // neighbouring pixels that share a column read it together (same addresses
   // in the same warp instruction) instead of a third of the walk apart.  The
   // certified sums are order-independent; every column is visited once.
-  __device__ __forceinline__ bool open(const ResliceArgs& a, uint32_t& visits) {
+  // pmask: the column phases (p = 3 jx + jy) this thread walks -- all 9, or
+  // with split pixels (small batches) those with p = part (mod 4).
+  __device__ __forceinline__ bool open(const ResliceArgs& a, uint32_t& visits, uint32_t pmask = 0x1ffu) {
     while (jx < 3) {
       while (cx <= hix) {
         while (cy <= hiy) {
@@ -432,10 +437,12 @@ struct FastWalk {
         cx += 3;
         cy = loy + (jy - loy % 3 + 3) % 3;
       }
-      if (++jy == 3) {
-        jy = 0;
-        ++jx;
-      }
+      do {
+        if (++jy == 3) {
+          jy = 0;
+          ++jx;
+        }
+      } while (jx < 3 && !((pmask >> (3 * jx + jy)) & 1u));
       cx = lox + (jx - lox % 3 + 3) % 3;
       cy = loy + (jy - loy % 3 + 3) % 3;
     }
@@ -527,13 +534,27 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 
 // Certified path: same mapping as reslice_k; branch-free f32 weights for
 // every visited record (no warp rounds), 4 loads in flight, phased walk.
-template <int kDistMode, int kGate>
+// kSplit (small pixel-major batches, where one pose's 16x16-pixel blocks
+// cannot fill the GPU): 4 threads per pixel, each walking the column phases
+// p = part (mod 4); the order-independent certified sums are combined with
+// shuffles.  Block = 8x8 pixels, warp = 4x2 pixels x 4 parts.
+template <int kDistMode, int kGate, bool kSplit>
 __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                       uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
-  map_pixel(a, pose, u, v, active);
+  const uint32_t part = kSplit ? (threadIdx.x & 3u) : 0u;
+  if (kSplit) {
+    const int warp = threadIdx.x >> 5, pl = (threadIdx.x & 31) >> 2;
+    pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+    u = (blockIdx.x % a.tiles_x) * 8 + (warp & 1) * 4 + (pl & 3);
+    v = (blockIdx.x / a.tiles_x) * 8 + (warp >> 1) * 2 + (pl >> 2);
+    active = u < a.W && v < a.H;
+  } else {
+    map_pixel(a, pose, u, v, active);
+  }
+  const uint32_t pmask = kSplit ? (0x111u << part) & 0x1ffu : 0x1ffu;
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
   const float g_single = kGate == kGateSingle ? __ldg(gate) : 0.0f;
   if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
@@ -569,9 +590,10 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     wl[1] = __double2float_rn(wy - (double)wh[1]);
     wl[2] = __double2float_rn(wz - (double)wh[2]);
     maxw = fmax(fabs(wx), fmax(fabs(wy), fabs(wz)));
-    w.jx = w.jy = 0;
-    w.cx = w.lox + (3 - w.lox % 3) % 3;
-    w.cy = w.loy + (3 - w.loy % 3) % 3;
+    w.jx = (int)part / 3;  // first phase of this thread (part < 4: phase = part)
+    w.jy = (int)part % 3;
+    w.cx = w.lox + (w.jx - w.lox % 3 + 3) % 3;
+    w.cy = w.loy + (w.jy - w.loy % 3 + 3) % 3;
     w.s = w.e = 0;
     live = active && w.lox <= w.hix && w.loy <= w.hiy && w.loz <= w.hiz;
     // quarters of cell loz below zlo and of cell hiz above zhi hold no survivor:
@@ -584,7 +606,7 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     }
   }
   uint32_t visits = 0;
-  if (live) live = w.open(a, visits);
+  if (live) live = w.open(a, visits, pmask);
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
   // batches of 4 record slots = 2 aligned pairs (256-bit loads); slots outside
@@ -603,11 +625,19 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     J += (double)bj;
     i0 += 4;
     if (i0 >= w.e) {
-      live = w.open(a, visits);
+      live = w.open(a, visits, pmask);
       i0 = w.s & ~1u;
     }
   }
-  if (!active) return;
+  if (kSplit) {  // the pixel's 4 partial sums (any order: the bound is order-free)
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      W += __shfl_xor_sync(0xffffffffu, W, o);
+      J += __shfl_xor_sync(0xffffffffu, J, o);
+      visits += __shfl_xor_sync(0xffffffffu, visits, o);
+    }
+  }
+  if (!active || part != 0) return;
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
   uint8_t ov, oc;
   if (certify(a, maxw, c2, W, J, visits, ov, oc)) {
@@ -619,12 +649,103 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
   }
 }
 
+// Latency-oriented form of exact_sums_warp for one pixel (all lanes hold the
+// same walk, fresh from init): the pixel's column runs (reference order:
+// columns x-major then y, cells loz..hiz inside each) are flattened into one
+// index space; lanes weigh 32 consecutive positions at a time with
+// independent loads, survivors are compacted IN ORDER into shared memory, and
+// one lane adds them sequentially -- the reference's sequence of FP64
+// additions.  Returns false (nothing written) when the pixel has more than 32
+// columns or more than `cap` survivors; the caller then uses exact_sums_warp.
+constexpr int kFlatCap = 256;  // survivors per warp held in shared memory
+
+template <int kDistMode>
+__device__ __forceinline__ bool exact_sums_flat(const Walk& w, const ResliceArgs& a, const double* gate,
+                                                double* sw, double* swi, double& wsum, double& iwsum) {
+  const int lane = threadIdx.x & 31;
+  wsum = 0.0;
+  iwsum = 0.0;
+  const bool empty = !(w.lox <= w.hix && w.loy <= w.hiy && w.loz <= w.hiz);
+  const int64_t ncy = empty ? 0 : w.hiy - w.loy + 1;
+  const int64_t ncol = empty ? 0 : (w.hix - w.lox + 1) * ncy;
+  if (ncol > 32) return false;
+  if (ncol == 0) return true;
+  uint32_t cs = 0, len = 0;
+  if (lane < ncol) {  // lane = column, in the reference's (cx, cy) order
+    const int64_t cx = w.lox + lane / ncy, cy = w.loy + lane % ncy;
+    const int64_t base = (cx * a.dims[1] + cy) * a.dims[2];
+    cs = __ldg(a.offsets + base + w.loz);
+    len = __ldg(a.offsets + base + w.hiz + 1) - cs;
+  }
+  uint32_t incl = len;  // inclusive prefix of run lengths over the columns
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t V = __shfl_sync(0xffffffffu, incl, (int)ncol - 1);
+  uint32_t cnt = 0;
+  constexpr int kU = 4;  // chunks of 32 positions in flight per iteration
+  for (uint32_t q0 = 0; q0 < V; q0 += 32 * kU) {  // warp-uniform trip count
+    uint4 c[kU];
+    bool in[kU];
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {  // issue every chunk's loads first
+      const uint32_t q = q0 + 32 * t + lane;
+      int lo = 0, hi = (int)ncol - 1;  // first column whose inclusive prefix exceeds q
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t pv = __shfl_sync(0xffffffffu, incl, mid);
+        if (lo < hi) {
+          if (q < pv) hi = mid;
+          else lo = mid + 1;
+        }
+      }
+      const uint32_t col_start = __shfl_sync(0xffffffffu, cs, lo);
+      const uint32_t col_excl = __shfl_sync(0xffffffffu, incl - len, lo);
+      in[t] = q < V;
+      c[t] = in[t] ? __ldg(a.records + canon_to_store(a.perm, col_start + (q - col_excl)))
+                   : make_uint4(0, 0, 0, 0);
+    }
+    bool keep[kU];
+    double wt[kU];
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {  // then the (independent) FP64 weights
+      keep[t] = in[t] && w.in_cube(c[t]) && gate[c[t].w >> 8] != CUDART_INF;
+      wt[t] = keep[t] ? exact_weight<kDistMode>(a, w, c[t], gate) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {  // and the in-order compaction
+      const unsigned m = __ballot_sync(0xffffffffu, keep[t]);
+      const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
+      if (keep[t] && pos < (uint32_t)kFlatCap) {
+        sw[pos] = wt[t];
+        swi[pos] = wt[t] * (double)(c[t].w & 0xffu);
+      }
+      cnt += __popc(m);
+    }
+  }
+  if (cnt > (uint32_t)kFlatCap) return false;
+  __syncwarp();
+  double ws = 0.0, is = 0.0;
+  if (lane == 0)
+    for (uint32_t i = 0; i < cnt; ++i) {
+      ws += sw[i];
+      is += swi[i];
+    }
+  wsum = ws;
+  iwsum = is;
+  return true;
+}
+
 // Exact recomputation of the pixels the certified path could not decide (all
 // pixels of the launch if the list overflowed): one warp per pixel, so a
 // handful of undecided pixels costs one short walk, not a serial one.
 template <int kDistMode>
 __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                        uint8_t* __restrict__ cov) {
+  __shared__ double s_w[8][kFlatCap], s_wi[8][kFlatCap];
   const unsigned n = *a.amb_count;
   const bool all = n > a.amb_cap;
   const uint64_t total = all ? (uint64_t)a.P * a.H * a.W : (uint64_t)n;
@@ -640,7 +761,10 @@ __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t
     Walk w;
     w.init(a, pose, u, v, true);
     double wsum, iwsum;
-    exact_sums_warp<kDistMode>(w, a, a.gate + (size_t)pose * a.n_orient, wsum, iwsum);
+    const double* gate = a.gate + (size_t)pose * a.n_orient;
+    const int wid = threadIdx.x >> 5;
+    if (!exact_sums_flat<kDistMode>(w, a, gate, s_w[wid], s_wi[wid], wsum, iwsum))
+      exact_sums_warp<kDistMode>(w, a, gate, wsum, iwsum);  // > 32 columns / many survivors
     if ((threadIdx.x & 31) == 0) write_exact(a, k, wsum, iwsum, out, cov);
   }
 }
@@ -802,34 +926,49 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   const bool fast = !brute && cfg->exact == 0 && a.lam > 0.0 && std::isfinite(a.c2) && fastmath_ok(s);
   const int tiles_y = (int)ceil_div(H, 16);
   PhaseTimer pt(s, "reslice");
-  Scratch<double> gate((size_t)P * a.n_orient, s);
-  Scratch<float> gate2((size_t)P * a.n_orient, s);
-  a.gate = gate.ptr;
-  a.gate2 = gate2.ptr;
-  if (vol->n_orient > 0) {
-    gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient,
-                                                                 d_params, P, *cfg, gate.ptr, gate2.ptr);
-    DARE_CUDA(cudaGetLastError());
-  }
-  pt.mark("gate");
-  a.order = nullptr;
   // auto: pose-major only helps the exact FP64 kernel on coherent trajectories;
   // the certified kernel's phased column walk shares loads better pixel-major
   // (cfg4: 16.8 vs 22.1 ms per 100 poses at 512^2)
   a.pose_major = (cfg->schedule == 2 || (cfg->schedule == 0 && coherent && !fast)) && !brute ? 1 : 0;
-  Scratch<int> order(P >= 4 ? P : 0, s);
-  if (P >= 4 && !brute && !a.pose_major) {
-    Scratch<unsigned long long> keys(2 * (size_t)P, s);
-    Scratch<int> idx(P, s);
+  const bool sorted = P >= 4 && !brute && !a.pose_major;
+  const uint64_t npix = (uint64_t)P * W * H;
+  // ambiguity list: 1/16 of the launch's pixels (overflow -> exact recompute of all)
+  a.amb_cap = fast ? (unsigned)std::min<uint64_t>(std::max<uint64_t>(npix / 16, 4096), 1u << 30) : 0u;
+  size_t sort_bytes = 0;
+  if (sorted)
+    DARE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned long long*)nullptr,
+                                              (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr,
+                                              P, 0, 60, s));
+  // all scratch of the launch in one block: the thread's arena on its own
+  // stream, one stream-ordered allocation on a caller's stream
+  const size_t n_gate = (size_t)P * a.n_orient;
+  const size_t total = Carve::up(n_gate * 8) + Carve::up(n_gate * 4) + Carve::up((size_t)P * 4) +
+                       Carve::up((size_t)P * 16) + Carve::up((size_t)P * 4) + Carve::up(sort_bytes) +
+                       Carve::up((size_t)a.amb_cap * 8) + Carve::up(4);
+  const bool arena = s == thread_stream() && total <= kArenaMax;
+  Scratch<uint8_t> block(arena ? 0 : total, s);
+  Carve cv{arena ? (uint8_t*)thread_arena(0, total, s) : block.ptr};
+  a.gate = cv.take<double>(n_gate);
+  a.gate2 = cv.take<float>(n_gate);
+  int* order = cv.take<int>(P);
+  unsigned long long* keys = cv.take<unsigned long long>(2 * (size_t)P);
+  int* idx = cv.take<int>(P);
+  uint8_t* tmp = cv.take<uint8_t>(sort_bytes);
+  a.amb = cv.take<unsigned long long>(a.amb_cap);
+  a.amb_count = cv.take<unsigned>(1);
+  if (vol->n_orient > 0) {
+    gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient,
+                                                                 d_params, P, *cfg, (double*)a.gate,
+                                                                 (float*)a.gate2);
+    DARE_CUDA(cudaGetLastError());
+  }
+  pt.mark("gate");
+  a.order = nullptr;
+  if (sorted) {
     pose_key_k<<<ceil_div(P, 128), 128, 0, s>>>(d_params, P, W, H, a.origin[0], a.origin[1],
-                                                 a.origin[2], 8.0 * a.voxel, keys.ptr, idx.ptr);
-    size_t bytes = 0;
-    DARE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.ptr, keys.ptr + P, idx.ptr,
-                                              order.ptr, P, 0, 60, s));
-    Scratch<uint8_t> tmp(bytes, s);
-    DARE_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, bytes, keys.ptr, keys.ptr + P, idx.ptr,
-                                              order.ptr, P, 0, 60, s));
-    a.order = order.ptr;
+                                                 a.origin[2], 8.0 * a.voxel, keys, idx);
+    DARE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, keys + P, idx, order, P, 0, 60, s));
+    a.order = order;
   }
   pt.mark("order");
   const dim3 grid = a.pose_major ? dim3(ceil_div(W, 4) * ceil_div(H, 2), ceil_div(P, 32))
@@ -839,12 +978,14 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_k<0>);
     set_smem(reslice_k<1>);
     set_smem(reslice_k<2>);
-    set_smem(reslice_fast_k<0, kGateGlobal>);
-    set_smem(reslice_fast_k<0, kGateSmem>);
-    set_smem(reslice_fast_k<0, kGateSingle>);
-    set_smem(reslice_fast_k<2, kGateGlobal>);
-    set_smem(reslice_fast_k<2, kGateSmem>);
-    set_smem(reslice_fast_k<2, kGateSingle>);
+    for (int sp = 0; sp < 2; ++sp) {
+      set_smem(sp ? reslice_fast_k<0, kGateGlobal, true> : reslice_fast_k<0, kGateGlobal, false>);
+      set_smem(sp ? reslice_fast_k<0, kGateSmem, true> : reslice_fast_k<0, kGateSmem, false>);
+      set_smem(sp ? reslice_fast_k<0, kGateSingle, true> : reslice_fast_k<0, kGateSingle, false>);
+      set_smem(sp ? reslice_fast_k<2, kGateGlobal, true> : reslice_fast_k<2, kGateGlobal, false>);
+      set_smem(sp ? reslice_fast_k<2, kGateSmem, true> : reslice_fast_k<2, kGateSmem, false>);
+      set_smem(sp ? reslice_fast_k<2, kGateSingle, true> : reslice_fast_k<2, kGateSingle, false>);
+    }
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -857,22 +998,28 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     DARE_CUDA(cudaGetLastError());
     return;
   }
-  // Ambiguity list: 1/16 of the launch's pixels (overflow -> exact recompute of all).
-  const uint64_t npix = (uint64_t)P * W * H;
-  a.amb_cap = (unsigned)std::min<uint64_t>(std::max<uint64_t>(npix / 16, 4096), 1u << 30);
-  Scratch<unsigned long long> amb(a.amb_cap, s);
-  Scratch<unsigned> amb_count(1, s);
-  a.amb = amb.ptr;
-  a.amb_count = amb_count.ptr;
-  DARE_CUDA(cudaMemsetAsync(amb_count.ptr, 0, sizeof(unsigned), s));
+  DARE_CUDA(cudaMemsetAsync(a.amb_count, 0, sizeof(unsigned), s));
   const int gmode = a.n_orient == 1 ? kGateSingle
                                     : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal);
-  auto k = a.dist_mode == 2
-               ? (gmode == kGateSingle ? reslice_fast_k<2, kGateSingle>
-                                       : (gmode == kGateSmem ? reslice_fast_k<2, kGateSmem> : reslice_fast_k<2, kGateGlobal>))
-               : (gmode == kGateSingle ? reslice_fast_k<0, kGateSingle>
-                                       : (gmode == kGateSmem ? reslice_fast_k<0, kGateSmem> : reslice_fast_k<0, kGateGlobal>));
-  k<<<grid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  // small pixel-major batches: split pixels over 4 threads (8x8-pixel blocks)
+  const bool split = !a.pose_major && P <= kSplitMaxPoses;
+  dim3 kgrid = grid;
+  if (split) {
+    a.tiles_x = (int)ceil_div(W, 8);
+    kgrid = dim3(a.tiles_x * ceil_div(H, 8), P);
+  }
+  auto pick = [&](auto dm) {
+    constexpr int D = decltype(dm)::value;
+    if (split)
+      return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, true>
+                                  : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, true>
+                                                        : reslice_fast_k<D, kGateGlobal, true>);
+    return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, false>
+                                : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, false>
+                                                      : reslice_fast_k<D, kGateGlobal, false>);
+  };
+  auto k = a.dist_mode == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
+  k<<<kgrid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");
   DARE_CUDA(cudaGetLastError());
   const unsigned fb_grid = (unsigned)sm_count() * 2;
@@ -933,23 +1080,28 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   if (n_poses == 0) return;
   cudaStream_t s = thread_stream();
   const size_t npix = (size_t)n_poses * width * height;
-  Scratch<double> d_params((size_t)n_poses * 14, s);
-  Scratch<uint8_t> d_out(2 * npix, s);
-  Scratch<unsigned long long> d_fb(1, s);
-  DARE_CUDA(cudaMemsetAsync(d_fb.ptr, 0, sizeof(unsigned long long), s));
-  DARE_CUDA(cudaMemcpyAsync(d_params.ptr, params, sizeof(double) * 14 * n_poses,
+  // call buffers from the thread's arena (slot 1; launch scratch uses slot 0)
+  const size_t total = Carve::up(sizeof(double) * 14 * n_poses) + Carve::up(2 * npix) +
+                       Carve::up(sizeof(unsigned long long));
+  Scratch<uint8_t> block(total > kArenaMax ? total : 0, s);
+  Carve cv{total > kArenaMax ? block.ptr : (uint8_t*)thread_arena(1, total, s)};
+  double* d_params = cv.take<double>((size_t)n_poses * 14);
+  uint8_t* d_out = cv.take<uint8_t>(2 * npix);
+  unsigned long long* d_fb = cv.take<unsigned long long>(1);
+  DARE_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), s));
+  DARE_CUDA(cudaMemcpyAsync(d_params, params, sizeof(double) * 14 * n_poses,
                             cudaMemcpyHostToDevice, s));
   for (int32_t p0 = 0; p0 < n_poses; p0 += 65535) {
     int32_t np = std::min<int32_t>(65535, n_poses - p0);
     size_t off = (size_t)p0 * width * height;
-    launch_reslice(vol, np, d_params.ptr + (size_t)p0 * 14, width, height, cfg, d_out.ptr + off,
-                   d_out.ptr + npix + off, s, brute,
-                   poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel), d_fb.ptr);
+    launch_reslice(vol, np, d_params + (size_t)p0 * 14, width, height, cfg, d_out + off,
+                   d_out + npix + off, s, brute,
+                   poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel), d_fb);
   }
   unsigned long long fb = 0;
-  DARE_CUDA(cudaMemcpyAsync(pixels, d_out.ptr, npix, cudaMemcpyDeviceToHost, s));
-  DARE_CUDA(cudaMemcpyAsync(coverage, d_out.ptr + npix, npix, cudaMemcpyDeviceToHost, s));
-  DARE_CUDA(cudaMemcpyAsync(&fb, d_fb.ptr, sizeof(fb), cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaMemcpyAsync(pixels, d_out, npix, cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaMemcpyAsync(coverage, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaMemcpyAsync(&fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
   tl_last_fallback = (int64_t)fb;
 }

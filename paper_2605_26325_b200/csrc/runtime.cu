@@ -45,6 +45,33 @@ void dev_alloc_bytes(void** p, size_t bytes) {
   DARE_CUDA(cudaStreamSynchronize(s));  // usable from any stream once this returns
 }
 
+void* thread_arena(int slot, size_t bytes, cudaStream_t s) {
+  struct Block {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  struct Arena {
+    std::map<std::pair<int, int>, Block> blocks;
+    ~Arena() {
+      for (auto& kv : blocks)
+        if (kv.second.p) cudaFree(kv.second.p);
+    }
+  };
+  static thread_local Arena arena;
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
+  Block& b = arena.blocks[{dev, slot}];
+  if (b.cap < bytes) {
+    if (b.p) DARE_CUDA(cudaFreeAsync(b.p, s));
+    b.p = nullptr;
+    b.cap = 0;
+    const size_t want = std::max(bytes, b.cap * 2);
+    DARE_CUDA(cudaMallocAsync(&b.p, want, s));
+    b.cap = want;
+  }
+  return b.p;
+}
+
 void dev_free(void* p) {
   if (!p) return;
   try {
