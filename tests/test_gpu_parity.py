@@ -368,15 +368,21 @@ def test_certified_path_equals_exact_path(rng):
             np.testing.assert_array_equal(fa[1], ex[1], err_msg=f"case {case} sched {sched}")
 
 
-def _lattice_volume(rng, n=24, spacing=0.125):
+def _lattice_volume(rng, n=24, spacing=0.125, checker=False):
     """Samples on an exact f32 lattice, one orientation, random intensities:
     equal weights (k_dist = 0) or symmetric distances make half-integer
-    weighted means common -- the cases the certified bound cannot decide."""
+    weighted means common -- the cases the certified bound cannot decide.
+    checker=True: intensity 10 + (x index mod 2), so any cube spanning an even
+    number of x lattice lines has a mean of exactly 10.5."""
     g = np.arange(n, dtype=np.float64) * spacing + spacing / 2
     pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
     q = np.tile([1.0, 0.0, 0.0, 0.0], (len(pos), 1))
     b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (n * spacing,) * 3), 0.25)
-    b.insert_batch(pos, q, rng.integers(0, 256, len(pos)))
+    if checker:
+        inten = 10 + (np.arange(len(pos)) // (n * n)) % 2
+    else:
+        inten = rng.integers(0, 256, len(pos))
+    b.insert_batch(pos, q, inten)
     return b.seal()
 
 
@@ -460,3 +466,24 @@ def test_certified_path_guard_rails(rng):
                              cfg.unassigned_value)
         np.testing.assert_array_equal(fa[0][0], ref[0])
         np.testing.assert_array_equal(fa[1][0].astype(bool), ref[1])
+
+
+@pytest.mark.parametrize("radius", [0.6, 1.1])
+def test_fallback_wide_neighbourhoods(rng, radius):
+    """Ties on a dense lattice with radii spanning 5 (25 columns, > 256
+    survivors per pixel: the flattened fallback overflows its shared-memory
+    capacity) and 9-10 cells per axis (> 32 columns): the fallback's general
+    warp walk must still reproduce the FP64 path bit for bit; single poses
+    (split-pixel certified kernel) and batches."""
+    vol = _lattice_volume(rng, checker=True)
+    planes = [ReslicePlane(Pose(Quaternion.identity(), (0.3, 0.2, 0.0625 + 0.25 * k)), 12, 10, (0.125, 0.125))
+              for k in range(6)]
+    cfg = ResliceConfig(interp_radius=radius, k_dist=0.0)
+    ex = _reslice_raw(vol, planes, cfg, True)
+    fa = _reslice_raw(vol, planes, cfg, False)
+    assert fa[2] > 0
+    np.testing.assert_array_equal(fa[0], ex[0])
+    np.testing.assert_array_equal(fa[1], ex[1])
+    one = _reslice_raw(vol, planes[:1], cfg, False)
+    np.testing.assert_array_equal(one[0][0], ex[0][0])
+    np.testing.assert_array_equal(one[1][0], ex[1][0])
