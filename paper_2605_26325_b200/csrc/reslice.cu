@@ -484,7 +484,7 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
   }
   const float wt = k ? ex2_approx(arg) : 0.0f;
   // intensity as f32 without I2F: bits 2^23 + I, minus 2^23 (exact)
-  const float inten = __fsub_rn(__uint_as_float(__byte_perm(c.w, 0x4B00u, 0x5440u)), 8388608.0f);
+  const float inten = __fsub_rn(__uint_as_float((c.w & 0xffu) | 0x4B000000u), 8388608.0f);
   bw = __fadd_rn(bw, wt);
   bj = __fmaf_rn(wt, inten, bj);
 }
@@ -618,9 +618,14 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     load_pair(a.records, i0 >> 1, r[0], r[1]);
     load_pair(a.records, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
     float bw = 0.0f, bj = 0.0f;
+    // slot i is in the run iff i < e - i0 (and, for slot 0 only, i0 >= s: the
+    // run starts at s or s - 1 rounded down to a pair)
+    const uint32_t rem = w.e - i0;
+    const bool first_ok = i0 >= w.s;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      fast_term<kDistMode, kGate>(r[i], i0 + i >= w.s && i0 + i < w.e, w, gate, g_single, wh, wl, c2, bw, bj);
+      fast_term<kDistMode, kGate>(r[i], (uint32_t)i < rem && (i > 0 || first_ok), w, gate, g_single, wh, wl,
+                                  c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
     i0 += 4;
