@@ -329,13 +329,19 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
   __shared__ SealSmem smem[kSealWarps];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   SealSmem& sm = smem[warp];
-  const uint32_t c0 = (blockIdx.x * kSealWarps + warp) * 32u;
-  if (c0 >= ncells) return;
+  // warp -> 32 consecutive cells of one column, z-chunk-major across warps:
+  // concurrently resident warps cover the same z range of many columns, so a
+  // z sweep's records come from the same few frames (L1-resident axes)
+  const uint32_t nz = (uint32_t)bo.nz, zchunks = (nz + 31u) / 32u, ncols = ncells / nz;
+  const uint32_t g = blockIdx.x * kSealWarps + warp;
+  const uint32_t zc = g / ncols, col = g - zc * ncols;
+  if (zc >= zchunks) return;
+  const uint32_t c0 = col * nz + zc * 32u;
   const uint32_t c = c0 + lane;
-  const uint32_t c_end = min(c0 + 32u, ncells);
+  const uint32_t c_end = min(c0 + 32u, col * nz + nz);
   const uint32_t s0 = offsets[c0], s1 = offsets[c_end];
   uint32_t cs = 0, cn = 0;
-  if (c < ncells) {
+  if (c < c_end) {
     cs = offsets[c];
     cn = offsets[c + 1] - cs;
   }
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       sm.slot[i] = (uint8_t)((z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]));
     }
     __syncwarp();
-    if (c < ncells) {  // lane = cell: stable destinations by bin, bins word
+    if (c < c_end) {  // lane = cell: stable destinations by bin, bins word
       const uint32_t r0 = cs - s0;
       uint32_t n[4] = {0, 0, 0, 0};
       for (uint32_t j = 0; j < cn; ++j) ++n[sm.slot[r0 + j]];
@@ -412,7 +418,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       bo.perm[cs + i] = 0;
     }
   }
-  if (!staged && c < ncells) {  // insertion order kept (big runs: sorted by the CUB path)
+  if (!staged && c < c_end) {  // insertion order kept (big runs: sorted by the CUB path)
     bo.bins[c] = 0;
     if (big)
       for (uint32_t i = 0; i < cn; ++i) bo.perm[cs + i] = 0;
@@ -496,7 +502,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                    carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
   }
-  seal_k<<<ceil_div(ncells, 32 * kSealWarps), 32 * kSealWarps, 0, s>>>(
+  seal_k<<<ceil_div((ncells / vol->dims[2]) * ceil_div(vol->dims[2], 32), kSealWarps), 32 * kSealWarps, 0, s>>>(
       rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr,
       BinOut{vol->origin[2], vol->voxel, vol->dims[2], vol->d_bins, vol->d_perm});
   DARE_CUDA(cudaGetLastError());
