@@ -5,9 +5,11 @@
 //              atomics, warp-aggregated over equal cells (integer sums are
 //              order-free, so atomics are exact -- baseline.py:67 relies on it);
 //              then values = f32(f64(sum) / f64(count)) (baseline.py:93-96).
-//  fill_holes: Jacobi passes on an f64 working grid (baseline.py:108: values
-//              are promoted to f64 and filled values are NOT re-rounded between
-//              passes).  Neighbour sums run in C order over the 26 offsets (the
+//  fill_holes: Jacobi passes in f64 (baseline.py:108: values are promoted to
+//              f64 and filled values are NOT re-rounded between passes).  Only
+//              voxels filled by this call need f64 storage (flag >= 3); every
+//              other value is read from the f32 input, whose promotion is
+//              exact.  Neighbour sums run in C order over the 26 offsets (the
 //              order scipy's convolve visits the footprint), unknown and
 //              out-of-grid neighbours add 0.  In-place with pass tags: a voxel
 //              filled in pass p carries flag 3+p and is "unknown" to readers in
@@ -114,11 +116,6 @@ __global__ void compound_finalize_k(int64_t n, const unsigned long long* __restr
   }
 }
 
-__global__ void to_f64_k(int64_t n, const float* __restrict__ v, double* w) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n) w[c] = (double)v[c];
-}
-
 // known in pass p: observed (1), filled earlier (2 or a tag from pass < p)
 __device__ __forceinline__ bool known_in_pass(uint8_t f, int tag) { return f != 0 && f != tag; }
 
@@ -132,10 +129,14 @@ constexpr int kFX = 4, kFY = 8, kFZ = 32;
 constexpr int kHX = kFX + 2, kHY = kFY + 2, kHZ = kFZ + 2;
 
 __global__ void __launch_bounds__(256) fill_pass_k(int64_t nx, int64_t ny, int64_t nz,
-                                                   double* v, uint8_t* flags, int tag,
-                                                   unsigned long long* filled,
-                                                   const unsigned long long* prev_filled) {
-  if (prev_filled && *prev_filled == 0) return;  // previous pass changed nothing
+                                                   const float* __restrict__ vin, double* v,
+                                                   uint8_t* flags, int tag,
+                                                   unsigned long long* filled, unsigned long long* left,
+                                                   const unsigned long long* prev_filled,
+                                                   const unsigned long long* prev_left) {
+  // previous pass changed nothing (no fillable voxel) or left no empty voxel
+  // (all known): the reference breaks out of its loop in both cases
+  if (prev_filled && (*prev_filled == 0 || *prev_left == 0)) return;
   __shared__ double s_val[kHX * kHY * kHZ];
   __shared__ uint8_t s_known[kHX * kHY * kHZ];
   const int64_t bz = (nz + kFZ - 1) / kFZ, by = (ny + kFY - 1) / kFY;
@@ -156,8 +157,9 @@ __global__ void __launch_bounds__(256) fill_pass_k(int64_t nx, int64_t ny, int64
     uint8_t kn = 0;
     if (X >= 0 && X < nx && Y >= 0 && Y < ny && Z >= 0 && Z < nz) {
       const int64_t q = (X * ny + Y) * nz + Z;
-      if (known_in_pass(((volatile uint8_t*)flags)[q], tag)) {
-        val = v[q];
+      const uint8_t f = ((volatile uint8_t*)flags)[q];
+      if (known_in_pass(f, tag)) {  // filled in an earlier pass: f64 work value; else the f32 input
+        val = f >= 3 ? ((volatile double*)v)[q] : (double)vin[q];
         kn = 1;
       }
     }
@@ -165,37 +167,62 @@ __global__ void __launch_bounds__(256) fill_pass_k(int64_t nx, int64_t ny, int64
     s_known[e] = kn;
   }
   __syncthreads();
-  bool did = false;
+  bool did = false, still_empty = false;
   for (int i = 0; i < kFX; ++i) {
     const int64_t x = x0 + i;
     if (x >= nx || y >= ny || z >= nz) continue;
     const int64_t c = (x * ny + y) * nz + z;
     if (flags[c] != 0) continue;
-    double s = 0.0, cnt = 0.0;
+    // the value sum stays FP64 in scipy's C order; the known count is a sum
+    // of <= 26 ones, exact in integers (identical to the FP64 convolution)
+    double s = 0.0;
+    int known_n = 0;
+#pragma unroll
     for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
       for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
         for (int dz = 0; dz < 3; ++dz) {
           if (dx == 1 && dy == 1 && dz == 1) continue;
           const int e = ((i + dx) * kHY + (ty + dy)) * kHZ + (tz + dz);
           s += s_val[e];
-          cnt += (double)s_known[e];
+          known_n += s_known[e];
         }
+    const double cnt = (double)known_n;
     if (cnt > 0.0) {
       v[c] = s / cnt;
       flags[c] = (uint8_t)tag;
       did = true;
+    } else {
+      still_empty = true;
     }
   }
   if (__syncthreads_or(did) && threadIdx.x == 0) atomicAdd(filled, 1ull);
+  if (__syncthreads_or(still_empty) && threadIdx.x == 0) atomicAdd(left, 1ull);
 }
 
-__global__ void fill_finalize_k(int64_t n, const double* __restrict__ v, const uint8_t* flags_in,
-                                float* values, uint8_t* flags) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  uint8_t f = flags_in[c];
-  values[c] = __double2float_rn(v[c]);
-  flags[c] = f >= 3 ? 2 : f;
+// 4 voxels per thread (u8 flags as one 32-bit word, values as float4)
+__global__ void fill_finalize_k(int64_t n, const float* __restrict__ vin, const double* __restrict__ v,
+                                const uint8_t* flags_in, float* values, uint8_t* flags) {
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c0 >= n) return;
+  if (c0 + 4 <= n) {
+    const uchar4 f = *reinterpret_cast<const uchar4*>(flags_in + c0);
+    float4 x = *reinterpret_cast<const float4*>(vin + c0);  // f32(f64(x)) == x unless refilled
+    if (f.x >= 3) x.x = __double2float_rn(v[c0]);
+    if (f.y >= 3) x.y = __double2float_rn(v[c0 + 1]);
+    if (f.z >= 3) x.z = __double2float_rn(v[c0 + 2]);
+    if (f.w >= 3) x.w = __double2float_rn(v[c0 + 3]);
+    *reinterpret_cast<float4*>(values + c0) = x;
+    *reinterpret_cast<uchar4*>(flags + c0) =
+        make_uchar4(f.x >= 3 ? 2 : f.x, f.y >= 3 ? 2 : f.y, f.z >= 3 ? 2 : f.z, f.w >= 3 ? 2 : f.w);
+    return;
+  }
+  for (int64_t c = c0; c < n; ++c) {
+    const uint8_t f = flags_in[c];
+    values[c] = f >= 3 ? __double2float_rn(v[c]) : vin[c];
+    flags[c] = f >= 3 ? 2 : f;
+  }
 }
 
 struct TrilinearArgs {
@@ -451,34 +478,41 @@ extern "C" int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar
     DARE_REQUIRE(in != nullptr && out != nullptr, "null argument");
     DARE_REQUIRE(max_passes >= 0 && max_passes <= 250, "max_passes must be in [0, 250]");
     cudaStream_t s = thread_stream();
+    PhaseTimer pt(s, "fill_holes");
     auto sv = new_scalar(in->origin, in->voxel, in->dims, in->d_counts != nullptr);
+    pt.mark("alloc_out");
     const int64_t n = in->ncells;
     Scratch<double> work(n, s);
     Scratch<uint8_t> flags(n, s);
-    Scratch<unsigned long long> filled(std::max(max_passes, 1), s);
-    DARE_CUDA(cudaMemsetAsync(filled.ptr, 0, sizeof(unsigned long long) * std::max(max_passes, 1), s));
+    Scratch<unsigned long long> filled(2 * std::max(max_passes, 1), s);  // per pass: filled, left
+    DARE_CUDA(cudaMemsetAsync(filled.ptr, 0, sizeof(unsigned long long) * 2 * std::max(max_passes, 1), s));
     DARE_CUDA(cudaMemcpyAsync(flags.ptr, in->d_flags, n, cudaMemcpyDeviceToDevice, s));
-    to_f64_k<<<ceil_div(n, 256), 256, 0, s>>>(n, in->d_values, work.ptr);
+    pt.mark("scratch");
     for (int p = 0; p < max_passes; ++p) {
       const unsigned fill_blocks = ceil_div(in->dims[0], kFX) * ceil_div(in->dims[1], kFY) *
                                    ceil_div(in->dims[2], kFZ);
-      fill_pass_k<<<fill_blocks, 256, 0, s>>>(in->dims[0], in->dims[1], in->dims[2],
-                                                    work.ptr, flags.ptr, 3 + p, filled.ptr + p,
-                                                    p ? filled.ptr + p - 1 : nullptr);
+      fill_pass_k<<<fill_blocks, 256, 0, s>>>(in->dims[0], in->dims[1], in->dims[2], in->d_values,
+                                                    work.ptr, flags.ptr, 3 + p, filled.ptr + 2 * p,
+                                                    filled.ptr + 2 * p + 1,
+                                                    p ? filled.ptr + 2 * p - 2 : nullptr,
+                                                    p ? filled.ptr + 2 * p - 1 : nullptr);
       DARE_CUDA(cudaGetLastError());
     }
-    fill_finalize_k<<<ceil_div(n, 256), 256, 0, s>>>(n, work.ptr, flags.ptr, sv->d_values,
-                                                     sv->d_flags);
+    pt.mark("passes");
+    fill_finalize_k<<<ceil_div(ceil_div(n, 4), 256), 256, 0, s>>>(n, in->d_values, work.ptr, flags.ptr,
+                                                                  sv->d_values, sv->d_flags);
     DARE_CUDA(cudaGetLastError());
+    pt.mark("finalize");
     if (in->d_counts)
       DARE_CUDA(cudaMemcpyAsync(sv->d_counts, in->d_counts, sizeof(int64_t) * n,
                                 cudaMemcpyDeviceToDevice, s));
-    std::vector<unsigned long long> h(std::max(max_passes, 1));
+    pt.mark("counts");
+    std::vector<unsigned long long> h(2 * std::max(max_passes, 1));
     DARE_CUDA(cudaMemcpyAsync(h.data(), filled.ptr, sizeof(unsigned long long) * h.size(),
                               cudaMemcpyDeviceToHost, s));
     DARE_CUDA(cudaStreamSynchronize(s));
     int32_t runs = 0;
-    for (int p = 0; p < max_passes; ++p) runs += h[p] > 0;
+    for (int p = 0; p < max_passes; ++p) runs += h[2 * p] > 0;
     if (passes_run) *passes_run = runs;
     *out = sv.release();
   });
