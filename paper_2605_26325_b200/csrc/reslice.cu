@@ -53,6 +53,7 @@ constexpr double kEps64 = 1.1102230246251565e-16;   // 2^-53
 constexpr double kEx2Err = 4.76837158203125e-07;    // 2^-21
 constexpr double kSqrtErr = 4.76837158203125e-07;   // 2^-21
 constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fast path accepts
+constexpr int kFastThreads = 128, kFastBlocks = 9;  // certified kernel: 36 warps/SM at 56 registers
 constexpr int kSplitMaxPoses = 4;      // pixel-major batches up to this size split pixels over 4 threads
 constexpr size_t kArenaMax = 256ull << 20;  // larger scratch uses stream-ordered allocations
 
@@ -405,8 +406,11 @@ __global__ void __launch_bounds__(256, 4) reslice_k(ResliceArgs a, uint8_t* __re
 // and no FP64 state in the loop (registers), columns visited in phases.
 struct FastWalk {
   float xlo, xhi, ylo, yhi, zlo, zhi;
-  int lox, hix, loy, hiy, loz, hiz, cx, cy, jx, jy;
-  int blo, bhi;  // first z quarter of cell loz / last z quarter of cell hiz that can hold a survivor
+  // loop-invariant walk state packed to keep registers for occupancy:
+  // cell ranges lo | hi << 16 per axis (dims < 2^15), cursor cx | cy << 16,
+  // phase and bins jx | jy << 2 | blo << 4 | bhi << 6 (blo: first z quarter of
+  // cell loz, bhi: last z quarter of cell hiz that can hold a survivor)
+  uint32_t xr, yr, zr, cur, ph;
   uint32_t s, e;
 
   // Columns in phases (cx mod 3, cy mod 3): within a phase, the 3x3
@@ -416,8 +420,13 @@ struct FastWalk {
   // pmask: the column phases (p = 3 jx + jy) this thread walks -- all 9, or
   // with split pixels (small batches) those with p = part (mod 4).
   __device__ __forceinline__ bool open(const ResliceArgs& a, uint32_t& visits, uint32_t pmask = 0x1ffu) {
-    while (jx < 3) {
-      while (cx <= hix) {
+    const int lox = xr & 0xffff, hix = (int)(xr >> 16) - 1, loy = yr & 0xffff, hiy = (int)(yr >> 16) - 1;
+    const int loz = zr & 0xffff, hiz = (int)(zr >> 16) - 1;
+    const int blo = (ph >> 4) & 3, bhi = (ph >> 6) & 3;
+    int cx = cur & 0xffff, cy = cur >> 16, jx = ph & 3, jy = (ph >> 2) & 3;
+    bool found = false;
+    while (jx < 3 && !found) {
+      while (cx <= hix && !found) {
         while (cy <= hiy) {
           // one contiguous storage range: drop the z quarters of the first and
           // last cell that lie wholly outside [zlo, zhi] (binned cells only)
@@ -431,12 +440,15 @@ struct FastWalk {
           cy += 3;
           if (s < e) {
             visits += e - s;
-            return true;
+            found = true;
+            break;
           }
         }
+        if (found) break;
         cx += 3;
         cy = loy + (jy - loy % 3 + 3) % 3;
       }
+      if (found) break;
       do {
         if (++jy == 3) {
           jy = 0;
@@ -446,7 +458,9 @@ struct FastWalk {
       cx = lox + (jx - lox % 3 + 3) % 3;
       cy = loy + (jy - loy % 3 + 3) % 3;
     }
-    return false;
+    cur = (uint32_t)cx | ((uint32_t)cy << 16);
+    ph = (ph & ~0xfu) | (uint32_t)jx | ((uint32_t)jy << 2);
+    return found;
   }
 
   __device__ __forceinline__ bool in_cube(const uint4& c) const {
@@ -539,20 +553,35 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 // p = part (mod 4); the order-independent certified sums are combined with
 // shuffles.  Block = 8x8 pixels, warp = 4x2 pixels x 4 parts.
 template <int kDistMode, int kGate, bool kSplit>
-__global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t* __restrict__ out,
-                                                      uint8_t* __restrict__ cov) {
+__global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(ResliceArgs a,
+                                                                           uint8_t* __restrict__ out,
+                                                                           uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
   const uint32_t part = kSplit ? (threadIdx.x & 3u) : 0u;
-  if (kSplit) {
-    const int warp = threadIdx.x >> 5, pl = (threadIdx.x & 31) >> 2;
-    pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
-    u = (blockIdx.x % a.tiles_x) * 8 + (warp & 1) * 4 + (pl & 3);
-    v = (blockIdx.x / a.tiles_x) * 8 + (warp >> 1) * 2 + (pl >> 2);
-    active = u < a.W && v < a.H;
-  } else {
-    map_pixel(a, pose, u, v, active);
+  {
+    // 4 warps per block: pixel-major 16x8 pixels (warp 8x4), split 8x4 pixels
+    // (warp 4x2 pixels x 4 parts), pose-major 4x1 pixels (warp = 32 poses)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (kSplit) {
+      const int pl = lane >> 2;
+      pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+      u = (blockIdx.x % a.tiles_x) * 8 + (warp & 1) * 4 + (pl & 3);
+      v = (blockIdx.x / a.tiles_x) * 4 + (warp >> 1) * 2 + (pl >> 2);
+      active = u < a.W && v < a.H;
+    } else if (a.pose_major) {
+      pose = blockIdx.y * 32 + lane;
+      u = (blockIdx.x % a.tiles_x) * 4 + warp;
+      v = blockIdx.x / a.tiles_x;
+      active = pose < a.P && u < a.W && v < a.H;
+      if (pose >= a.P) pose = a.P - 1;
+    } else {
+      pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+      u = (blockIdx.x % a.tiles_x) * 16 + (warp & 1) * 8 + (lane & 7);
+      v = (blockIdx.x / a.tiles_x) * 8 + (warp >> 1) * 4 + (lane >> 3);
+      active = u < a.W && v < a.H;
+    }
   }
   const uint32_t pmask = kSplit ? (0x111u << part) & 0x1ffu : 0x1ffu;
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
@@ -565,7 +594,6 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
   }
   FastWalk w;
   float wh[3], wl[3];
-  double maxw;
   bool live;
   {
     const double* pp = a.params + (size_t)pose * 14;
@@ -575,13 +603,10 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     const double wz = (pp[2] + du * pp[9]) + dv * pp[10];
     const double r = a.radius;
     const double inv_v = 1.0 / a.voxel;
-    int64_t lo, hi;
-    cell_range(wx, r, a.origin[0], inv_v, a.dims[0], lo, hi);
-    w.lox = (int)lo, w.hix = (int)hi;
-    cell_range(wy, r, a.origin[1], inv_v, a.dims[1], lo, hi);
-    w.loy = (int)lo, w.hiy = (int)hi;
-    cell_range(wz, r, a.origin[2], inv_v, a.dims[2], lo, hi);
-    w.loz = (int)lo, w.hiz = (int)hi;
+    int64_t xlo_c, xhi_c, ylo_c, yhi_c, zlo_c, zhi_c;
+    cell_range(wx, r, a.origin[0], inv_v, a.dims[0], xlo_c, xhi_c);
+    cell_range(wy, r, a.origin[1], inv_v, a.dims[1], ylo_c, yhi_c);
+    cell_range(wz, r, a.origin[2], inv_v, a.dims[2], zlo_c, zhi_c);
     w.xlo = keep_lo(wx, r), w.xhi = keep_hi(wx, r);
     w.ylo = keep_lo(wy, r), w.yhi = keep_hi(wy, r);
     w.zlo = keep_lo(wz, r), w.zhi = keep_hi(wz, r);
@@ -589,21 +614,24 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     wl[0] = __double2float_rn(wx - (double)wh[0]);
     wl[1] = __double2float_rn(wy - (double)wh[1]);
     wl[2] = __double2float_rn(wz - (double)wh[2]);
-    maxw = fmax(fabs(wx), fmax(fabs(wy), fabs(wz)));
-    w.jx = (int)part / 3;  // first phase of this thread (part < 4: phase = part)
-    w.jy = (int)part % 3;
-    w.cx = w.lox + (w.jx - w.lox % 3 + 3) % 3;
-    w.cy = w.loy + (w.jy - w.loy % 3 + 3) % 3;
-    w.s = w.e = 0;
-    live = active && w.lox <= w.hix && w.loy <= w.hiy && w.loz <= w.hiz;
+    live = active && xlo_c <= xhi_c && ylo_c <= yhi_c && zlo_c <= zhi_c;
+    // hi + 1 is stored (an empty range's hi can be -1); dims < 2^15 (host check)
+    w.xr = (uint32_t)xlo_c | ((uint32_t)(xhi_c + 1) << 16);
+    w.yr = (uint32_t)ylo_c | ((uint32_t)(yhi_c + 1) << 16);
+    w.zr = (uint32_t)zlo_c | ((uint32_t)(zhi_c + 1) << 16);
     // quarters of cell loz below zlo and of cell hiz above zhi hold no survivor:
     // bin b holds zb(b) <= z < zb(b+1), so b < blo => z < zb(blo) <= zlo, and
     // b > bhi => z >= zb(bhi+1) > zhi (exact f32 comparisons).
-    w.blo = w.bhi = 0;
+    uint32_t blo = 0, bhi = 0;
     for (int k = 1; k <= 3; ++k) {
-      w.blo += zbin_bound(a.origin[2], a.voxel, w.loz, k) <= w.zlo;
-      w.bhi += zbin_bound(a.origin[2], a.voxel, w.hiz, k) <= w.zhi;
+      blo += zbin_bound(a.origin[2], a.voxel, zlo_c, k) <= w.zlo;
+      bhi += zbin_bound(a.origin[2], a.voxel, zhi_c, k) <= w.zhi;
     }
+    const uint32_t jx = part / 3, jy = part % 3;  // first phase of this thread (part < 4: phase = part)
+    const int64_t cx0 = xlo_c + ((int64_t)jx - xlo_c % 3 + 3) % 3, cy0 = ylo_c + ((int64_t)jy - ylo_c % 3 + 3) % 3;
+    w.cur = (uint32_t)cx0 | ((uint32_t)cy0 << 16);
+    w.ph = jx | (jy << 2) | (blo << 4) | (bhi << 6);
+    w.s = w.e = 0;
   }
   uint32_t visits = 0;
   if (live) live = w.open(a, visits, pmask);
@@ -643,6 +671,13 @@ __global__ void __launch_bounds__(256, 4) reslice_fast_k(ResliceArgs a, uint8_t*
     }
   }
   if (!active || part != 0) return;
+  double maxw;  // recomputed here rather than kept live through the walk (registers)
+  {
+    const double* pp = a.params + (size_t)pose * 14;
+    const double du = (double)u * pp[12], dv = (double)v * pp[13];
+    maxw = fmax(fabs((pp[0] + du * pp[3]) + dv * pp[4]),
+                fmax(fabs((pp[1] + du * pp[6]) + dv * pp[7]), fabs((pp[2] + du * pp[9]) + dv * pp[10])));
+  }
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
   uint8_t ov, oc;
   if (certify(a, maxw, c2, W, J, visits, ov, oc)) {
@@ -928,7 +963,9 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.amb_count = nullptr;
   a.amb_cap = 0;
   a.fallback_total = d_fallback_total;
-  const bool fast = !brute && cfg->exact == 0 && a.lam > 0.0 && std::isfinite(a.c2) && fastmath_ok(s);
+  // (the certified walker packs cell indices in 16 bits)
+  const bool fast = !brute && cfg->exact == 0 && a.lam > 0.0 && std::isfinite(a.c2) && a.dims[0] < 32768 &&
+                    a.dims[1] < 32768 && a.dims[2] < 32768 && fastmath_ok(s);
   const int tiles_y = (int)ceil_div(H, 16);
   PhaseTimer pt(s, "reslice");
   // auto: pose-major only helps the exact FP64 kernel on coherent trajectories;
@@ -1006,11 +1043,17 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   DARE_CUDA(cudaMemsetAsync(a.amb_count, 0, sizeof(unsigned), s));
   const int gmode = a.n_orient == 1 ? kGateSingle
                                     : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal);
-  // small pixel-major batches: split pixels over 4 threads (8x8-pixel blocks)
+  // small pixel-major batches: split pixels over 4 threads
   const bool split = !a.pose_major && P <= kSplitMaxPoses;
-  dim3 kgrid = grid;
+  dim3 kgrid;
   if (split) {
     a.tiles_x = (int)ceil_div(W, 8);
+    kgrid = dim3(a.tiles_x * ceil_div(H, 4), P);
+  } else if (a.pose_major) {
+    a.tiles_x = (int)ceil_div(W, 4);
+    kgrid = dim3(a.tiles_x * H, ceil_div(P, 32));
+  } else {
+    a.tiles_x = (int)ceil_div(W, 16);
     kgrid = dim3(a.tiles_x * ceil_div(H, 8), P);
   }
   auto pick = [&](auto dm) {
@@ -1024,7 +1067,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
                                                       : reslice_fast_k<D, kGateGlobal, false>);
   };
   auto k = a.dist_mode == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
-  k<<<kgrid, 256, kSmemBytes, s>>>(a, d_pixels, d_cov);
+  k<<<kgrid, kFastThreads, kSmemBytes, s>>>(a, d_pixels, d_cov);
   pt.mark("reslice_fast_k");
   DARE_CUDA(cudaGetLastError());
   const unsigned fb_grid = (unsigned)sm_count() * 2;
