@@ -258,25 +258,27 @@ __global__ void __launch_bounds__(256) trilinear_k(TrilinearArgs a, uint8_t* out
     i[k] = (int64_t)(fl < -2.0 ? -2.0 : (fl > lim ? lim : fl));
     fr[k] = g - fl;
   }
+  // all 8 corners' loads first (independent), then the reference's
+  // (cx, cy, cz) accumulation order (_kernels.py:205-221)
+  uint8_t fl8[8];
+  float val8[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int64_t jx = i[0] + (c >> 2), jy = i[1] + ((c >> 1) & 1), jz = i[2] + (c & 1);
+    const bool in = jx >= 0 && jx < a.dims[0] && jy >= 0 && jy < a.dims[1] && jz >= 0 && jz < a.dims[2];
+    const int64_t lin = in ? (jx * a.dims[1] + jy) * a.dims[2] + jz : 0;
+    fl8[c] = in ? __ldg(a.flags + lin) : (uint8_t)0;
+    val8[c] = in ? __ldg(a.values + lin) : 0.0f;
+  }
   double wsum = 0.0, vsum = 0.0;
-  for (int cx = 0; cx < 2; ++cx) {
-    const int64_t jx = i[0] + cx;
-    if (jx < 0 || jx >= a.dims[0]) continue;
-    const double wxc = cx == 1 ? fr[0] : 1.0 - fr[0];
-    for (int cy = 0; cy < 2; ++cy) {
-      const int64_t jy = i[1] + cy;
-      if (jy < 0 || jy >= a.dims[1]) continue;
-      const double wyc = cy == 1 ? fr[1] : 1.0 - fr[1];
-      for (int cz = 0; cz < 2; ++cz) {
-        const int64_t jz = i[2] + cz;
-        if (jz < 0 || jz >= a.dims[2]) continue;
-        const int64_t lin = (jx * a.dims[1] + jy) * a.dims[2] + jz;
-        if (__ldg(a.flags + lin) != 0) {
-          const double wc = (wxc * wyc) * (cz == 1 ? fr[2] : 1.0 - fr[2]);
-          wsum += wc;
-          vsum += wc * (double)__ldg(a.values + lin);
-        }
-      }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (fl8[c] != 0) {
+      const double wxc = (c >> 2) ? fr[0] : 1.0 - fr[0];
+      const double wyc = ((c >> 1) & 1) ? fr[1] : 1.0 - fr[1];
+      const double wc = (wxc * wyc) * ((c & 1) ? fr[2] : 1.0 - fr[2]);
+      wsum += wc;
+      vsum += wc * (double)val8[c];
     }
   }
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
