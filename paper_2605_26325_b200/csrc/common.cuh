@@ -60,6 +60,7 @@ int guard(F&& body) {
 // One non-blocking stream per (host thread, device): concurrent reslice calls
 // from different threads never serialise on a shared stream.
 cudaStream_t thread_stream();
+cudaStream_t thread_copy_stream();  // companion stream for overlapped host<->device copies
 
 // Stream-ordered device scratch (cudaMallocAsync pool) freed on scope exit.
 template <class T>

@@ -149,7 +149,8 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
 }
 
 template <bool kFill, bool kInv>
-__global__ void __launch_bounds__(256) frame_run_k(FrameView fv, VoxelMap m, uint32_t* counts,
+__global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begin, uint32_t f_end,
+                                                   VoxelMap m, uint32_t* counts,
                                                    const uint32_t* __restrict__ offsets,
                                                    unsigned long long* keys,
                                                    unsigned long long* rejected) {
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, VoxelMap m, uin
   const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
   const uint32_t p = v * fv.W + u;
   const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
-  const uint32_t f0 = blockIdx.y * kRunFrames;
-  const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
+  const uint32_t f0 = f_begin + blockIdx.y * kRunFrames;
+  const int nf = (int)min((uint32_t)kRunFrames, f_end - f0);
   for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[(size_t)f0 * 9 + i];
   if (kFill)
     for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (uint32_t)fv.image[f0 + i];
@@ -583,17 +584,25 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                                 cudaMemcpyHostToDevice, s));
     }
     DARE_LIMIT(ceil_div(n_frames, kRunFrames) <= 65535, "too many frames for one launch");
-    const dim3 grid(ceil_div(width, 16) * ceil_div(height, 16),
-                    (unsigned)std::max<int64_t>(ceil_div(n_frames, kRunFrames), 1));
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
                        unsigned long long* keys, unsigned long long* rej) {
       if (n_frames == 0) return;
-      if (fill)
-        (m.exact_inv ? frame_run_k<true, true> : frame_run_k<true, false>)<<<grid, 256, 0, s>>>(
-            fv, m, counts, offsets, keys, rej);
-      else
-        (m.exact_inv ? frame_run_k<false, true> : frame_run_k<false, false>)<<<grid, 256, 0, s>>>(
-            fv, m, counts, offsets, keys, rej);
+      const unsigned tiles = ceil_div(width, 16) * ceil_div(height, 16);
+      if (!fill) {  // needs no intensities: runs while host frames are still uploading
+        (m.exact_inv ? frame_run_k<false, true> : frame_run_k<false, false>)<<<
+            dim3(tiles, (unsigned)ceil_div(n_frames, kRunFrames)), 256, 0, s>>>(
+            fv, 0u, (uint32_t)n_frames, m, counts, offsets, keys, rej);
+        return;
+      }
+      // fill in groups of frames, each launched once its images are resident
+      const int64_t step = fs.done.empty() ? n_frames : (int64_t)kRunFrames * 32;
+      for (int64_t f0 = 0; f0 < n_frames; f0 += step) {
+        const int64_t f1 = std::min<int64_t>(n_frames, f0 + step);
+        fs.wait_frames(s, f0, f1);
+        (m.exact_inv ? frame_run_k<true, true> : frame_run_k<true, false>)<<<
+            dim3(tiles, (unsigned)ceil_div(f1 - f0, kRunFrames)), 256, 0, s>>>(
+            fv, (uint32_t)f0, (uint32_t)f1, m, counts, offsets, keys, rej);
+      }
     };
     Scratch<SealAxes> sa((size_t)std::max<int64_t>(n_frames, 1), s);
     if (n_frames > 0) {
@@ -601,6 +610,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
       DARE_CUDA(cudaGetLastError());
     }
     // measured: cfg3 (8000 frames, 576 KB of axes) seal 52.3 -> 46.0 ms at 75%
+    fs.start_upload();  // after the small uploads above (they would queue behind the frames)
     build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s,
               n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1);
     DARE_CUDA(cudaStreamSynchronize(s));

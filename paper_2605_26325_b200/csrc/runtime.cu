@@ -39,6 +39,25 @@ cudaStream_t thread_stream() {
   return s;
 }
 
+cudaStream_t thread_copy_stream() {
+  // Second per-(thread, device) stream for host<->device copies overlapping compute.
+  struct Streams {
+    std::map<int, cudaStream_t> by_dev;
+    ~Streams() {
+      for (auto& kv : by_dev) cudaStreamDestroy(kv.second);
+    }
+  };
+  static thread_local Streams streams;
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
+  auto it = streams.by_dev.find(dev);
+  if (it != streams.by_dev.end()) return it->second;
+  cudaStream_t s;
+  DARE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  streams.by_dev[dev] = s;
+  return s;
+}
+
 void dev_alloc_bytes(void** p, size_t bytes) {
   cudaStream_t s = thread_stream();
   DARE_CUDA(cudaMallocAsync(p, bytes ? bytes : 1, s));
@@ -151,8 +170,12 @@ FrameSet::FrameSet(const uint8_t* frames, int64_t n_images, int32_t H_, int32_t 
   } else {
     size_t bytes = hw * (size_t)n_images;
     if (bytes) {
+      // grouped upload on the copy stream (start_upload): the count pass (which
+      // needs no intensities) and the early fill launches overlap the transfer
       DARE_CUDA(cudaMallocAsync((void**)&owned_frames, bytes, s));
-      DARE_CUDA(cudaMemcpyAsync(owned_frames, frames, bytes, cudaMemcpyHostToDevice, s));
+      h_frames = frames;
+      this->n_images = n_images;
+      h_image.assign(frame_image, frame_image + n_frames);
     }
     d_frames = owned_frames;
   }
@@ -170,7 +193,38 @@ FrameSet::FrameSet(const uint8_t* frames, int64_t n_images, int32_t H_, int32_t 
   }
 }
 
+void FrameSet::start_upload() {
+  if (!h_frames || !done.empty()) return;
+  const size_t hw = (size_t)H * W;
+  cudaEvent_t ready;
+  DARE_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  DARE_CUDA(cudaEventRecord(ready, stream));  // allocation visible to the copy stream
+  cudaStream_t cs = thread_copy_stream();
+  DARE_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  DARE_CUDA(cudaEventDestroy(ready));
+  const int64_t groups = std::min<int64_t>(8, n_images);
+  per_group = (n_images + groups - 1) / groups;
+  for (int64_t g = 0; g * per_group < n_images; ++g) {
+    const int64_t i0 = g * per_group, i1 = std::min(n_images, i0 + per_group);
+    DARE_CUDA(cudaMemcpyAsync(owned_frames + hw * (size_t)i0, h_frames + hw * (size_t)i0,
+                              hw * (size_t)(i1 - i0), cudaMemcpyHostToDevice, cs));
+    cudaEvent_t e;
+    DARE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    DARE_CUDA(cudaEventRecord(e, cs));
+    done.push_back(e);
+  }
+}
+
+void FrameSet::wait_frames(cudaStream_t s, int64_t f_begin, int64_t f_end) const {
+  if (done.empty() || f_begin >= f_end) return;
+  int32_t last = 0;
+  for (int64_t f = f_begin; f < f_end; ++f) last = std::max(last, h_image[f]);
+  DARE_CUDA(cudaStreamWaitEvent(s, done[std::min<size_t>(last / per_group, done.size() - 1)], 0));
+}
+
 FrameSet::~FrameSet() {
+  if (!done.empty()) cudaStreamWaitEvent(stream, done.back(), 0);  // copies finished before the free
+  for (cudaEvent_t e : done) cudaEventDestroy(e);
   if (owned_frames) cudaFreeAsync(owned_frames, stream);
   if (d_image) cudaFreeAsync(d_image, stream);
   if (d_axes) cudaFreeAsync(d_axes, stream);

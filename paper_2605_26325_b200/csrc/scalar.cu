@@ -358,6 +358,8 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
     FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
                 frame_axes, pitch_x, pitch_y, mask, s);
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
+    fs.start_upload();
+    fs.wait_frames(s, 0, n_frames);  // host frames: every image uploaded before compound_k reads them
     ScalarFrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, fs.n_frames,
                        fs.H,        fs.W,       fs.px,     fs.py};
     const int64_t hw = (int64_t)height * width;

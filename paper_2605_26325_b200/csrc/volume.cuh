@@ -98,9 +98,21 @@ struct FrameSet {
   double px = 0, py = 0;
   uint8_t* owned_frames = nullptr;
   cudaStream_t stream = nullptr;
+  // host frames are uploaded in groups of images on the thread's copy stream;
+  // group g (images [g * per_group, ...)) is resident once done[g] completed
+  std::vector<cudaEvent_t> done;
+  int64_t per_group = 0;
+  std::vector<int32_t> h_image;  // frame -> image (host copy, for wait_frames)
+  const uint8_t* h_frames = nullptr;
+  int64_t n_images = 0;
   FrameSet(const uint8_t* frames, int64_t n_images, int32_t H, int32_t W, int32_t on_device,
            const int32_t* frame_image, int64_t n_frames, const double* axes, double px, double py,
            const uint8_t* mask, cudaStream_t s);
+  // start the grouped upload of host frames -- after every small (pageable)
+  // upload of the call, which would otherwise queue behind it on the copy engine
+  void start_upload();
+  // make `s` wait until the images of frames [f_begin, f_end) are on the device
+  void wait_frames(cudaStream_t s, int64_t f_begin, int64_t f_end) const;
   ~FrameSet();
 };
 
