@@ -11,8 +11,9 @@
 //              counted (volume.py:230-233).
 //   2. scan  : exclusive prefix of counts -> cell offsets (CUB).
 //   3. fill  : same runs -> slots = offset + atomic cursor; stores the 64-bit
-//              key (insertion index << 8 | intensity); the insertion index is
-//              synchronized frame * H*W + row-major pixel.
+//              key (insertion index << 10 | z bin << 8 | intensity); the
+//              insertion index orders like synchronized frame * H*W + row-major
+//              pixel (bit-packed (frame, v, u) when the widths fit 32 bits).
 //   4. seal  : per cell, sort its (tiny) key run ascending = insertion order --
 //              this is what makes the atomic fill identical to numpy's stable
 //              argsort -- and materialise the 16 B records.  A warp seals 32
@@ -60,7 +61,32 @@ struct FrameView {
   double px, py;
   const uint32_t* oid;  // orientation id per synchronized frame
   FastDiv div_w, div_hw;
+  // insertion index encoding in the keys: packed (f << fshift | v << ushift | u)
+  // when the bit widths fit 32 bits -- same order as f * hw + v * W + u, decoded
+  // with shifts in the seal -- else linear (f * hw + p, decoded with FastDiv)
+  uint32_t packed, ushift, fshift, fstride;
+  __device__ __forceinline__ uint32_t pixel_key(uint32_t u, uint32_t v) const {
+    return packed ? (v << ushift) | u : v * W + u;
+  }
+  __device__ __forceinline__ void decode(uint32_t pid, uint32_t& f, uint32_t& u, uint32_t& v) const {
+    if (packed) {
+      f = pid >> fshift;
+      v = (pid >> ushift) & ((1u << (fshift - ushift)) - 1u);
+      u = pid & ((1u << ushift) - 1u);
+    } else {
+      f = div_hw.div(pid);
+      const uint32_t p = pid - f * hw;
+      v = div_w.div(p);
+      u = p - v * W;
+    }
+  }
 };
+
+static inline uint32_t ceil_log2(uint64_t x) {
+  uint32_t l = 0;
+  while ((1ull << l) < x) ++l;
+  return l;
+}
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
@@ -101,23 +127,34 @@ __device__ __forceinline__ void warp_scatter(bool kept, int32_t lin, unsigned lo
 constexpr int kRunFrames = 64;
 constexpr int kMaxRun = 8;  // intensities buffered in two u32
 
+// Sort keys: insertion index << kKeyShift | z bin << 8 | low byte (intensity for
+// frames).  The z bin (z quarter of the cell, volume.cuh) rides in bits 8-9 so
+// the seal need not recompute z; it sits below the index, so key order is
+// insertion order.
+constexpr int kKeyShift = 10;
+
 template <bool kInv>
-__device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, double V, const VoxelMap& m) {
+__device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, double V, const VoxelMap& m,
+                                                float& z32, uint32_t& iz) {
   bool ok = true;
   uint32_t idx[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double d = (double)__double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]) - m.origin[a];
+    const float p32 = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
+    if (a == 2) z32 = p32;
+    const double d = (double)p32 - m.origin[a];
     const double f = floor(kInv ? d * m.inv_voxel : d / m.voxel);
     ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
     idx[a] = ok ? (uint32_t)f : 0u;
   }
+  iz = idx[2];
   return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
 }
 
 template <bool kFill>
 __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, uint32_t run_f,
-                                          uint32_t ib0, uint32_t ib1, uint32_t p, uint32_t hw,
+                                          uint32_t ib0, uint32_t ib1, uint32_t bb, uint32_t pk,
+                                          uint32_t fstride,
                                           uint32_t* counts, const uint32_t* __restrict__ offsets,
                                           unsigned long long* keys) {
   const unsigned lane = lane_id();
@@ -142,7 +179,8 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
       unsigned long long* dst = keys + offsets[lin] + base + prefix;
       for (uint32_t t = 0; t < k; ++t) {
         const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
-        dst[t] = ((unsigned long long)((run_f + t) * hw + p) << 8) | inten;
+        dst[t] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
+                 (((bb >> (2 * t)) & 3u) << 8) | inten;
       }
     }
   }
@@ -160,7 +198,7 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
   const uint32_t tiles_u = (fv.W + 15) / 16;
   const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
   const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const uint32_t p = v * fv.W + u;
+  const uint32_t p = v * fv.W + u, pk = fv.pixel_key(u, v);
   const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
   const uint32_t f0 = f_begin + blockIdx.y * kRunFrames;
   const int nf = (int)min((uint32_t)kRunFrames, f_end - f0);
@@ -170,9 +208,12 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
   __syncthreads();
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   int32_t cur = -1;
-  uint32_t run_f = 0, k = 0, ib0 = 0, ib1 = 0;
+  uint32_t run_f = 0, k = 0, ib0 = 0, ib1 = 0, bb = 0;
+  float zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;  // z-quarter bounds of the run's cell (fill)
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count
-    const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m) : -1;
+    float z = 0.f;
+    uint32_t iz = 0;
+    const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m, z, iz) : -1;
     if (!kFill) {
       const unsigned oob = __ballot_sync(0xffffffffu, in_frame && lin < 0);
       if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
@@ -180,14 +221,20 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     const bool need = restart && cur >= 0;
     if (__any_sync(0xffffffffu, need))
-      run_flush<kFill>(need, cur, k, run_f, ib0, ib1, p, fv.hw, counts, offsets, keys);
+      run_flush<kFill>(need, cur, k, run_f, ib0, ib1, bb, pk, fv.fstride, counts, offsets, keys);
     if (restart) {
       cur = lin;
       run_f = f0 + j;
       k = 0;
-      ib0 = ib1 = 0;
+      ib0 = ib1 = bb = 0;
+      if (kFill && lin >= 0) {
+        zb1 = zbin_bound(m.origin[2], m.voxel, iz, 1);
+        zb2 = zbin_bound(m.origin[2], m.voxel, iz, 2);
+        zb3 = zbin_bound(m.origin[2], m.voxel, iz, 3);
+      }
     }
     if (kFill && lin >= 0) {
+      bb |= (uint32_t)((z >= zb1) + (z >= zb2) + (z >= zb3)) << (2 * k);
       const uint32_t inten = fv.frames[(size_t)s_img[j] * fv.hw + p];
       if (k < 4) ib0 |= inten << (8 * k);
       else ib1 |= inten << (8 * (k - 4));
@@ -196,10 +243,11 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
   }
   const bool need = cur >= 0;
   if (__any_sync(0xffffffffu, need))
-    run_flush<kFill>(need, cur, k, run_f, ib0, ib1, p, fv.hw, counts, offsets, keys);
+    run_flush<kFill>(need, cur, k, run_f, ib0, ib1, bb, pk, fv.fstride, counts, offsets, keys);
 }
 
-// Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index << 8.
+// Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index
+// << kKeyShift (no z bin: the seal computes it from the positions).
 template <bool kFill>
 __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict__ pos, int64_t n,
                                                         VoxelMap m, uint32_t* counts,
@@ -225,7 +273,7 @@ __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict_
     const int oob = __syncthreads_count(valid && !kept);
     if (threadIdx.x == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
   }
-  warp_scatter<kFill>(kept, lin, (unsigned long long)i << 8, counts, offsets, keys);
+  warp_scatter<kFill>(kept, lin, (unsigned long long)i << kKeyShift, counts, offsets, keys);
 }
 
 // Seal-side frame table (80 B per frame): per axis a the pair (R[a][0],
@@ -253,11 +301,12 @@ __global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __r
 }
 
 struct FrameRecords {
+  static constexpr bool kKeyBins = true;  // z bins computed by the fill pass
   FrameView fv;
   const SealAxes* sa;
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t inten) const {
-    const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
-    const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
+    uint32_t f, u, v;
+    fv.decode(pid, f, u, v);
     const SealAxes& x = sa[f];
     const double U = (double)u * fv.px, V = (double)v * fv.py;
     float p32[3];
@@ -271,8 +320,8 @@ struct FrameRecords {
   }
   // z only (the binning key), same arithmetic as operator()
   __device__ __forceinline__ float z_of(uint32_t pid) const {
-    const uint32_t f = fv.div_hw.div(pid), p = pid - f * fv.hw;
-    const uint32_t v = fv.div_w.div(p), u = p - v * fv.W;
+    uint32_t f, u, v;
+    fv.decode(pid, f, u, v);
     const double2 r = sa[f].r[2];
     const double U = (double)u * fv.px, V = (double)v * fv.py;
     return __double2float_rn((U * r.x + V * r.y) + sa[f].t[2]);
@@ -280,6 +329,7 @@ struct FrameRecords {
 };
 
 struct SampleRecords {
+  static constexpr bool kKeyBins = false;
   const float* pos;
   const uint32_t* word;  // (oid << 8) | intensity
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t) const {
@@ -295,12 +345,11 @@ constexpr int kSealWarps = 4;  // warps per seal block
 constexpr int kPitch = 33;     // odd row pitch: both access patterns conflict-free
 
 struct SealSmem {
-  uint32_t st[kSmallRun * kPitch];             // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
-  uint8_t si[kSmallRun * kPitch];              // its low key byte (intensity for frames)
-  uint16_t cstart[32];                         // cell start relative to the warp's first key
-  uint8_t cell_of[kSmallRun * 32];             // key position -> lane of its cell (0xff: big run)
-  uint8_t slot[kSmallRun * 32];                // key position -> z bin, then destination in its cell
-  float zb[3][32];                             // z-quarter boundaries of each lane's cell
+  uint32_t st[kSmallRun * kPitch];  // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
+  uint16_t sx[kSmallRun * kPitch];  // its low key byte | z bin << 8, later | destination << 8
+  uint16_t cstart[32];              // cell start relative to the warp's first key
+  uint8_t cell_of[kSmallRun * 32];  // key position -> lane of its cell
+  float zb[3][32];                  // z-quarter boundaries of each lane's cell (SampleRecords)
 };
 
 // z-quarter binning of the sealed runs (layout in volume.cuh)
@@ -353,53 +402,72 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
   if (staged) {
     sm.cstart[lane] = (uint16_t)(cs - s0);
     for (uint32_t k = 0; k < cn; ++k) sm.cell_of[cs - s0 + k] = (uint8_t)lane;
-    __syncwarp();
-    for (uint32_t i = lane; i < len; i += 32) {
-      const uint32_t col = sm.cell_of[i];
-      // key = insertion index << 8 | byte: staged as u32 + u8 (smaller stage, more warps)
-      const unsigned long long key = keys[s0 + i];
-      const uint32_t at = (i - sm.cstart[col]) * kPitch + col;
-      sm.st[at] = (uint32_t)(key >> 8);
-      sm.si[at] = (uint8_t)key;
-    }
-    __syncwarp();
-    for (uint32_t i = 1; i < cn; ++i) {  // by insertion index; the byte moves along
-      const uint32_t x = sm.st[i * kPitch + lane];
-      const uint8_t xi = sm.si[i * kPitch + lane];
-      uint32_t j = i;
-      while (j > 0 && sm.st[(j - 1) * kPitch + lane] > x) {
-        sm.st[j * kPitch + lane] = sm.st[(j - 1) * kPitch + lane];
-        sm.si[j * kPitch + lane] = sm.si[(j - 1) * kPitch + lane];
-        --j;
-      }
-      sm.st[j * kPitch + lane] = x;
-      sm.si[j * kPitch + lane] = xi;
-    }
-    {
+    if constexpr (!Rec::kKeyBins) {
       const int64_t iz = (int64_t)c % bo.nz;
 #pragma unroll
       for (int q = 0; q < 3; ++q) sm.zb[q][lane] = zbin_bound(bo.oz, bo.voxel, iz, q + 1);
     }
     __syncwarp();
-    for (uint32_t i = lane; i < len; i += 32) {  // z bin of every sealed sample
-      const uint32_t col = sm.cell_of[i];
-      const float z = rec.z_of(sm.st[(i - sm.cstart[col]) * kPitch + col]);  // insertion index
-      sm.slot[i] = (uint8_t)((z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]));
+    // keys staged as u32 index + u16 (byte | z bin << 8): smaller stage, more
+    // warps.  Four loads in flight per lane; keys are read once (streaming, L1
+    // kept for the frame-axes lookups of the record pass)
+    for (uint32_t i0 = 0; i0 < len; i0 += 128) {
+      unsigned long long kk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t i = i0 + 32u * q + lane;
+        kk[q] = i < len ? __ldcs(keys + s0 + i) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t i = i0 + 32u * q + lane;
+        if (i < len) {
+          const uint32_t col = sm.cell_of[i];
+          const uint32_t at = (i - sm.cstart[col]) * kPitch + col;
+          const uint32_t pid = (uint32_t)(kk[q] >> kKeyShift);
+          uint32_t bin;
+          if constexpr (Rec::kKeyBins) {
+            bin = (uint32_t)(kk[q] >> 8) & 3u;
+          } else {
+            const float z = rec.z_of(pid);
+            bin = (z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]);
+          }
+          sm.st[at] = pid;
+          sm.sx[at] = (uint16_t)((kk[q] & 0xffu) | (bin << 8));
+        }
+      }
     }
     __syncwarp();
+    for (uint32_t i = 1; i < cn; ++i) {  // by insertion index; byte and bin move along
+      const uint32_t x = sm.st[i * kPitch + lane];
+      const uint16_t xs = sm.sx[i * kPitch + lane];
+      uint32_t j = i;
+      while (j > 0 && sm.st[(j - 1) * kPitch + lane] > x) {
+        sm.st[j * kPitch + lane] = sm.st[(j - 1) * kPitch + lane];
+        sm.sx[j * kPitch + lane] = sm.sx[(j - 1) * kPitch + lane];
+        --j;
+      }
+      sm.st[j * kPitch + lane] = x;
+      sm.sx[j * kPitch + lane] = xs;
+    }
     if (c < c_end) {  // lane = cell: stable destinations by bin, bins word
-      const uint32_t r0 = cs - s0;
-      uint32_t n[4] = {0, 0, 0, 0};
-      for (uint32_t j = 0; j < cn; ++j) ++n[sm.slot[r0 + j]];
-      uint32_t next[4] = {0, n[0], n[0] + n[1], n[0] + n[1] + n[2]};
-      for (uint32_t j = 0; j < cn; ++j) sm.slot[r0 + j] = (uint8_t)(next[sm.slot[r0 + j]]++);
-      bo.bins[c] = n[0] | ((n[0] + n[1]) << 8) | ((n[0] + n[1] + n[2]) << 16) | (1u << 24);
+      // per-bin counters packed as bytes (runs <= 32): registers, not local memory
+      uint32_t n = 0;
+      for (uint32_t j = 0; j < cn; ++j) n += 1u << (8u * (sm.sx[j * kPitch + lane] >> 8));
+      const uint32_t c1 = n & 0xffu, c2 = c1 + ((n >> 8) & 0xffu), c3 = c2 + ((n >> 16) & 0xffu);
+      uint32_t next = (c1 << 8) | (c2 << 16) | (c3 << 24);  // byte b = first slot of bin b
+      for (uint32_t j = 0; j < cn; ++j) {
+        const uint32_t w = sm.sx[j * kPitch + lane], sh = 8u * (w >> 8);
+        sm.sx[j * kPitch + lane] = (uint16_t)((w & 0xffu) | (((next >> sh) & 0xffu) << 8));
+        next += 1u << sh;
+      }
+      bo.bins[c] = c1 | (c2 << 8) | (c3 << 16) | (1u << 24);
     }
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t col = sm.cell_of[i];
-      const uint32_t j = i - sm.cstart[col], dest = sm.slot[i];
-      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col], sm.si[j * kPitch + col]);
+      const uint32_t j = i - sm.cstart[col], w = sm.sx[j * kPitch + col], dest = w >> 8;
+      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col], w & 0xffu);
       bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
   } else if (cn > 0 && !big) {
@@ -415,7 +483,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       k[j] = x;
     }
     for (uint32_t i = 0; i < cn; ++i) {
-      records[cs + i] = rec((uint32_t)(k[i] >> 8), (uint32_t)(k[i] & 0xffu));
+      records[cs + i] = rec((uint32_t)(k[i] >> kKeyShift), (uint32_t)(k[i] & 0xffu));
       bo.perm[cs + i] = 0;
     }
   }
@@ -442,7 +510,7 @@ __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_
                                   const unsigned long long* __restrict__ sorted, uint4* records) {
   uint32_t b = begins[blockIdx.x], e = ends[blockIdx.x];
   for (uint32_t s = b + threadIdx.x; s < e; s += blockDim.x)
-    records[s] = rec((uint32_t)(sorted[s] >> 8), (uint32_t)(sorted[s] & 0xffu));
+    records[s] = rec((uint32_t)(sorted[s] >> kKeyShift), (uint32_t)(sorted[s] & 0xffu));
 }
 
 // count -> scan -> fill -> seal, shared by frames and arbitrary samples.
@@ -576,7 +644,16 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                               cudaMemcpyHostToDevice, s));
     FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
                  (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
-                 FastDiv((uint32_t)width), FastDiv((uint32_t)hw)};
+                 FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw};
+    {
+      const uint32_t ub = ceil_log2((uint64_t)width), vb = ceil_log2((uint64_t)height);
+      if (ub + vb + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 32 && ub + vb < 32) {
+        fv.packed = 1;
+        fv.ushift = ub;
+        fv.fshift = ub + vb;
+        fv.fstride = 1u << (ub + vb);
+      }
+    }
     vol->n_orient = (int64_t)table.size();
     if (!table.empty()) {
       dev_alloc(&vol->d_orient, sizeof(float4) * table.size());

@@ -12,6 +12,7 @@ not elementwise numpy.
 from __future__ import annotations
 
 import math
+import operator
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -131,18 +132,22 @@ class FramePlan:
         px, py = self.pixel_pitch
         umax = (self.width - 1) * px
         vmax = (self.height - 1) * py
-        lo = np.full(3, np.inf)
-        hi = np.full(3, -np.inf)
-        for u, v in ((0.0, 0.0), (umax, 0.0), (0.0, vmax), (umax, vmax)):
-            c = geo.rotate_many(self.rotations, np.array([u, v, 0.0])) + self.translations
-            lo = np.minimum(lo, c.min(axis=0))
-            hi = np.maximum(hi, c.max(axis=0))
-        return BoundingBox(lo, hi).expanded(margin)
+        corners = np.array([(0.0, 0.0, 0.0), (umax, 0.0, 0.0), (0.0, vmax, 0.0), (umax, vmax, 0.0)])
+        c = geo.rotate_grid(self.rotations, corners) + self.translations[:, None, :]
+        return BoundingBox(c.min(axis=(0, 1)), c.max(axis=(0, 1))).expanded(margin)
+
+
+_wxyz = operator.attrgetter("w", "x", "y", "z")
 
 
 def _quat_array(poses) -> np.ndarray:
-    return np.array([[p.rotation.w, p.rotation.x, p.rotation.y, p.rotation.z] for p in poses],
-                    dtype=float).reshape(-1, 4)
+    return np.array([_wxyz(p.rotation) for p in poses], dtype=float).reshape(-1, 4)
+
+
+def _translation_array(poses) -> np.ndarray:
+    if not poses:
+        return np.zeros((0, 3))
+    return np.concatenate([p.translation for p in poses]).astype(float, copy=False).reshape(-1, 3)
 
 
 def plan_frames(sweep) -> FramePlan:
@@ -170,7 +175,7 @@ def plan_frames(sweep) -> FramePlan:
     mq = np.empty((len(kept), 4))
     mt = np.empty((len(kept), 3))
     all_q = _quat_array(poses)
-    all_t = np.array([np.asarray(p.translation, dtype=float) for p in poses]).reshape(-1, 3)
+    all_t = _translation_array(poses)
     mq[exact] = all_q[idx[exact]]
     mt[exact] = all_t[idx[exact]]
     for j in np.nonzero(~exact)[0]:

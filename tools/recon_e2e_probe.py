@@ -11,3 +11,10 @@ for i in range(4):
     print(f"e2e {1e3*(t1-t0):.2f} ms", file=sys.stderr)
     del v
 t0 = time.perf_counter(); x = pinned.cuda(); torch.cuda.synchronize(); print(f"plain H2D {1e3*(time.perf_counter()-t0):.2f} ms", file=sys.stderr)
+# frames already in HBM (bench `recon.ms` path)
+swd = bench.host_sweep(wl, frames_d)  # images as a CUDA tensor
+for i in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    v = db.reconstruct_volume(swd, voxel_size=wl.voxel, margin=0.0); torch.cuda.synchronize()
+    print(f"device-frames {1e3*(time.perf_counter()-t0):.2f} ms", file=sys.stderr)
+    del v
