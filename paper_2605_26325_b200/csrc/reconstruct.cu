@@ -187,7 +187,7 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
 }
 
 template <bool kFill, bool kInv>
-__global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begin, uint32_t f_end,
+__global__ void __launch_bounds__(256, 5) frame_run_k(FrameView fv, uint32_t f_begin, uint32_t f_end,
                                                    VoxelMap m, uint32_t* counts,
                                                    const uint32_t* __restrict__ offsets,
                                                    unsigned long long* keys,
@@ -210,7 +210,11 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
   int32_t cur = -1;
   uint32_t run_f = 0, k = 0, ib0 = 0, ib1 = 0, bb = 0;
   float zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;  // z-quarter bounds of the run's cell (fill)
+  // intensities loaded one frame ahead (latency hidden behind the frame's math)
+  uint32_t inten_next = (kFill && in_frame && nf > 0) ? fv.frames[(size_t)s_img[0] * fv.hw + p] : 0u;
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count
+    const uint32_t inten = inten_next;
+    if (kFill && in_frame && j + 1 < nf) inten_next = fv.frames[(size_t)s_img[j + 1] * fv.hw + p];
     float z = 0.f;
     uint32_t iz = 0;
     const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m, z, iz) : -1;
@@ -235,7 +239,6 @@ __global__ void __launch_bounds__(256) frame_run_k(FrameView fv, uint32_t f_begi
     }
     if (kFill && lin >= 0) {
       bb |= (uint32_t)((z >= zb1) + (z >= zb2) + (z >= zb3)) << (2 * k);
-      const uint32_t inten = fv.frames[(size_t)s_img[j] * fv.hw + p];
       if (k < 4) ib0 |= inten << (8 * k);
       else ib1 |= inten << (8 * (k - 4));
     }

@@ -18,3 +18,9 @@ for i in range(3):
     v = db.reconstruct_volume(swd, voxel_size=wl.voxel, margin=0.0); torch.cuda.synchronize()
     print(f"device-frames {1e3*(time.perf_counter()-t0):.2f} ms", file=sys.stderr)
     del v
+# host-side planning alone (synchronize + bounds + per-frame axes/quaternions)
+from paper_2605_26325_b200 import sweep as _sw
+for i in range(3):
+    t0 = time.perf_counter(); plan = _sw.plan_frames(swd); g = _sw.grid_for(plan, wl.voxel, 0.0)
+    plan.axes(); plan.canonical_quats_f32()
+    print(f"host plan {1e3*(time.perf_counter()-t0):.2f} ms", file=sys.stderr)
