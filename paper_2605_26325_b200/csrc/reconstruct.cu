@@ -118,11 +118,11 @@ __device__ __forceinline__ void warp_scatter(bool kept, int32_t lin, unsigned lo
 // synchronized frames; warp = an 8(u) x 4(v) patch, block = 16 x 16 pixels.
 // Consecutive frames of a sweep put a pixel into the same cell for several
 // frames, so each thread keeps a run (cell, first frame, length <= kMaxRun,
-// the run's intensities) and only flushes when the cell changes; a flush is
-// warp-aggregated over lanes flushing the same cell (image neighbours): one
-// atomic per group, ranks inside the group from a bit-sliced ballot prefix of
-// the run lengths.  Count pass: u32 histogram; fill pass: slot = cell offset +
-// returned cursor + rank, keys written for every sample of the run.  (Slot
+// the run's intensities) and only flushes when the cell changes.  Count pass:
+// one u32 reduction per run.  Fill pass: the flush is warp-aggregated over
+// lanes flushing the same cell (image neighbours): one atomic per group, ranks
+// inside the group from a bit-sliced ballot prefix of the run lengths; slot =
+// cell offset + returned cursor + rank, keys written for every sample of the run.  (Slot
 // order inside a cell is irrelevant: seal sorts every run by insertion key.)
 constexpr int kRunFrames = 64;
 constexpr int kMaxRun = 8;  // intensities buffered in two u32
@@ -158,6 +158,10 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
                                           uint32_t* counts, const uint32_t* __restrict__ offsets,
                                           unsigned long long* keys) {
   const unsigned lane = lane_id();
+  if (!kFill) {  // count pass: plain reductions (measured faster than the MATCH grouping)
+    if (need) atomicAdd(&counts[lin], k);
+    return;
+  }
   // lanes not flushing get a key no cell has, so MATCH runs on the full warp
   const unsigned peers = __match_any_sync(0xffffffffu, need ? (unsigned)lin : (0x80000000u | lane));
   const unsigned lt = (1u << lane) - 1u;
@@ -169,19 +173,15 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
     prefix += (unsigned)__popc(mb & lt) << b;
   }
   const unsigned leader = __ffs(peers) - 1;
-  if (!kFill) {
-    if (need && lane == leader) atomicAdd(&counts[lin], total);
-  } else {
-    unsigned base = 0;
-    if (need && lane == leader) base = atomicAdd(&counts[lin], total);
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (need) {
-      unsigned long long* dst = keys + offsets[lin] + base + prefix;
-      for (uint32_t t = 0; t < k; ++t) {
-        const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
-        dst[t] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
-                 (((bb >> (2 * t)) & 3u) << 8) | inten;
-      }
+  unsigned base = 0;
+  if (need && lane == leader) base = atomicAdd(&counts[lin], total);
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (need) {  // the group's runs take consecutive slots: coalesced key stores
+    unsigned long long* dst = keys + offsets[lin] + base + prefix;
+    for (uint32_t t = 0; t < k; ++t) {
+      const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
+      dst[t] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
+               (((bb >> (2 * t)) & 3u) << 8) | inten;
     }
   }
 }
