@@ -172,16 +172,25 @@ __device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, ui
     total += (unsigned)__popc(mb) << b;
     prefix += (unsigned)__popc(mb & lt) << b;
   }
+  // Groups whose runs cover the same frames (the common case: image neighbours
+  // crossing a cell together) take their slots frame-major -- (frame, pixel)
+  // = insertion order -- so the seal's per-cell sort finds them presorted.
   const unsigned leader = __ffs(peers) - 1;
+  const uint32_t fk = (run_f << 4) | k;
+  const uint32_t leader_fk = __shfl_sync(0xffffffffu, fk, leader);  // all lanes (full mask)
+  const bool differs = need && leader_fk != fk;
+  const bool uniform = (__ballot_sync(0xffffffffu, differs) & peers) == 0u;
   unsigned base = 0;
   if (need && lane == leader) base = atomicAdd(&counts[lin], total);
   base = __shfl_sync(0xffffffffu, base, leader);
   if (need) {  // the group's runs take consecutive slots: coalesced key stores
-    unsigned long long* dst = keys + offsets[lin] + base + prefix;
+    const unsigned n = __popc(peers), rank = __popc(peers & lt);
+    unsigned long long* dst = keys + offsets[lin] + base + (uniform ? rank : prefix);
+    const uint32_t stride = uniform ? n : 1u;
     for (uint32_t t = 0; t < k; ++t) {
       const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
-      dst[t] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
-               (((bb >> (2 * t)) & 3u) << 8) | inten;
+      dst[t * stride] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
+                        (((bb >> (2 * t)) & 3u) << 8) | inten;
     }
   }
 }
@@ -279,14 +288,18 @@ __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict_
   warp_scatter<kFill>(kept, lin, (unsigned long long)i << kKeyShift, counts, offsets, keys);
 }
 
-// Seal-side frame table (80 B per frame): per axis a the pair (R[a][0],
-// R[a][1]) as one 16 B load plus t[a], and the orientation id -- 7 loads per
-// record instead of 10 (the seal is bound by L1 wavefronts on these lookups).
-struct SealAxes {
-  double2 r[3];
-  double t[3];
+// Seal-side frame table (96 B per frame, 32 B aligned): the axis pairs
+// (R[a][0], R[a][1]) and t in two 256-bit loads, t[2] + orientation id in one
+// 128-bit load -- 3 loads per record instead of 10 (the seal is bound by L1
+// wavefronts on these lookups).
+struct __align__(32) SealAxes {
+  double r0x, r0y, r1x, r1y;  // load A
+  double r2x, r2y, t0, t1;    // load B
+  double t2;                  // load C: t2 | oid
   uint32_t oid, pad;
+  double pad2[2];
 };
+static_assert(sizeof(SealAxes) == 96, "SealAxes layout");
 
 __global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __restrict__ oid,
                             uint32_t n, SealAxes* out) {
@@ -294,13 +307,30 @@ __global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __r
   if (f >= n) return;
   const double* fa = axes + (size_t)f * 9;
   SealAxes x;
-  for (int a = 0; a < 3; ++a) {
-    x.r[a] = make_double2(fa[a], fa[3 + a]);
-    x.t[a] = fa[6 + a];
-  }
+  x.r0x = fa[0];
+  x.r0y = fa[3];
+  x.r1x = fa[1];
+  x.r1y = fa[4];
+  x.r2x = fa[2];
+  x.r2y = fa[5];
+  x.t0 = fa[6];
+  x.t1 = fa[7];
+  x.t2 = fa[8];
   x.oid = oid[f];
   x.pad = 0;
+  x.pad2[0] = x.pad2[1] = 0.0;
   out[f] = x;
+}
+
+__device__ __forceinline__ void ld256_f64(const void* p, double& a, double& b, double& c, double& d) {
+  uint32_t w[8];
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+      : "l"(p));
+  a = __hiloint2double((int)w[1], (int)w[0]);
+  b = __hiloint2double((int)w[3], (int)w[2]);
+  c = __hiloint2double((int)w[5], (int)w[4]);
+  d = __hiloint2double((int)w[7], (int)w[6]);
 }
 
 struct FrameRecords {
@@ -310,24 +340,27 @@ struct FrameRecords {
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t inten) const {
     uint32_t f, u, v;
     fv.decode(pid, f, u, v);
-    const SealAxes& x = sa[f];
+    const SealAxes* x = sa + f;
+    double r0x, r0y, r1x, r1y, r2x, r2y, t0, t1;
+    ld256_f64(&x->r0x, r0x, r0y, r1x, r1y);
+    ld256_f64(&x->r2x, r2x, r2y, t0, t1);
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(&x->t2));
+    const double t2 = __hiloint2double((int)c.y, (int)c.x);
     const double U = (double)u * fv.px, V = (double)v * fv.py;
-    float p32[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {  // reconstruct.py:156-162: ((U*R[a,0]) + (V*R[a,1])) + t[a]
-      const double2 r = x.r[a];
-      p32[a] = __double2float_rn((U * r.x + V * r.y) + x.t[a]);
-    }
-    return make_uint4(__float_as_uint(p32[0]), __float_as_uint(p32[1]), __float_as_uint(p32[2]),
-                      (x.oid << 8) | inten);
+    // reconstruct.py:156-162: ((U*R[a,0]) + (V*R[a,1])) + t[a]
+    const float p0 = __double2float_rn((U * r0x + V * r0y) + t0);
+    const float p1 = __double2float_rn((U * r1x + V * r1y) + t1);
+    const float p2 = __double2float_rn((U * r2x + V * r2y) + t2);
+    return make_uint4(__float_as_uint(p0), __float_as_uint(p1), __float_as_uint(p2),
+                      (c.z << 8) | inten);
   }
   // z only (the binning key), same arithmetic as operator()
   __device__ __forceinline__ float z_of(uint32_t pid) const {
     uint32_t f, u, v;
     fv.decode(pid, f, u, v);
-    const double2 r = sa[f].r[2];
+    const SealAxes& x = sa[f];
     const double U = (double)u * fv.px, V = (double)v * fv.py;
-    return __double2float_rn((U * r.x + V * r.y) + sa[f].t[2]);
+    return __double2float_rn((U * x.r2x + V * x.r2y) + x.t2);
   }
 };
 
@@ -441,15 +474,23 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
       }
     }
     __syncwarp();
-    for (uint32_t i = 1; i < cn; ++i) {  // by insertion index; byte and bin move along
+    // by insertion index (unique); byte and bin move along.  `top` = the
+    // largest key so far: presorted runs (frame-major fill) cost one load each
+    uint32_t top = cn ? sm.st[lane] : 0u;
+    for (uint32_t i = 1; i < cn; ++i) {
       const uint32_t x = sm.st[i * kPitch + lane];
+      if (x > top) {
+        top = x;
+        continue;
+      }
       const uint16_t xs = sm.sx[i * kPitch + lane];
       uint32_t j = i;
-      while (j > 0 && sm.st[(j - 1) * kPitch + lane] > x) {
-        sm.st[j * kPitch + lane] = sm.st[(j - 1) * kPitch + lane];
+      uint32_t y = top;  // st[j - 1] for j = i
+      do {
+        sm.st[j * kPitch + lane] = y;
         sm.sx[j * kPitch + lane] = sm.sx[(j - 1) * kPitch + lane];
         --j;
-      }
+      } while (j > 0 && (y = sm.st[(j - 1) * kPitch + lane]) > x);
       sm.st[j * kPitch + lane] = x;
       sm.sx[j * kPitch + lane] = xs;
     }
