@@ -716,7 +716,9 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
         return;
       }
       // fill in groups of frames, each launched once its images are resident
-      const int64_t step = fs.done.empty() ? n_frames : (int64_t)kRunFrames * 32;
+      // (one launch per upload group, so fill overlaps the rest of the transfer)
+      const int64_t step = fs.done.empty() ? n_frames
+                                           : std::max<int64_t>(kRunFrames, ceil_div(fs.per_group, kRunFrames) * kRunFrames);
       for (int64_t f0 = 0; f0 < n_frames; f0 += step) {
         const int64_t f1 = std::min<int64_t>(n_frames, f0 + step);
         fs.wait_frames(s, f0, f1);
