@@ -180,6 +180,15 @@ int dare_volume_destroy(dare_volume_t vol);
 int dare_reslice(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
                  int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
                  uint8_t* coverage);
+/* Service form of dare_reslice (service.py:273-293 process_request, which
+ * reslices one request and ships protocol.pack_coverage(image.coverage),
+ * protocol.py:273-274): same pixels; coverage bit-packed on the device per pose
+ * in np.packbits order (MSB first), ceil(height*width/8) bytes per pose, so the
+ * device->host copy carries 1/8 of the coverage bytes.  Host buffers:
+ * pixels n_poses x height x width, coverage_bits n_poses x ceil(h*w/8). */
+int dare_reslice_packed(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
+                        int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
+                        uint8_t* coverage_bits);
 /* Contract twin of reslice (reslice.py:190-205 -> _kernels.reslice_rows_bruteforce
  * 142-167): every sample in storage order for every pixel.  Host buffers. */
 int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const double* params,

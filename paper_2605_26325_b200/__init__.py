@@ -9,7 +9,9 @@ Drop-in surface (same names, signatures, defaults, errors as the reference):
   ScalarVolume, ReslicePlane, ResliceConfig, ResliceImage, SweepRecording,
   save/load_volume, save/load_scalar_volume, geometry types.
 B200 extensions: reslice_batch, reslice_trilinear_batch (many poses per
-launch), reconstruct_volume(frames_device_ptr=...), parallel.* (multi-GPU).
+launch), reconstruct_volume(frames_device_ptr=...), parallel.* (multi-GPU),
+service.ResliceBatcher / reslice_packed (service request path: concurrent
+requests coalesced into batched launches, coverage bit-packed on device).
 """
 from .errors import (
     DareError,
@@ -45,6 +47,7 @@ from .reslice import (
     sample_weight,
 )
 from .reconstruct import reconstruct_volume
+from .service import ResliceBatcher, reslice_packed
 from .scalar import (
     VOXEL_EMPTY,
     VOXEL_FILLED,

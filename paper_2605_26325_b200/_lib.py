@@ -84,6 +84,7 @@ _SIGNATURES = {
     "dare_volume_get_info": [c_vp, ctypes.POINTER(VolumeInfo)],
     "dare_volume_destroy": [c_vp],
     "dare_reslice": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
+    "dare_reslice_packed": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_bruteforce": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8,
                                 P_u8],
     "dare_poses_coherent": [P_f64, c_i32, c_i32, c_i32, c_f64],

@@ -1118,10 +1118,25 @@ static bool poses_coherent(const double* p, int32_t P, int32_t W, int32_t H, dou
   return close >= (int)(0.9 * (P - 1));
 }
 
+// Coverage bit-packed per pose in np.packbits order (protocol.py:273-274: MSB
+// first, the pose's last byte zero-padded): thread = one output byte.
+__global__ void pack_coverage_k(const uint8_t* __restrict__ cov, int64_t hw, int64_t bytes_per_pose,
+                                int64_t n_bytes, uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_bytes) return;
+  const int64_t p = i / bytes_per_pose, j = i - p * bytes_per_pose;
+  const uint8_t* c = cov + p * hw + 8 * j;
+  const int64_t n = hw - 8 * j < 8 ? hw - 8 * j : 8;
+  uint32_t b = 0;
+  for (int k = 0; k < n; ++k) b |= (c[k] != 0 ? 1u : 0u) << (7 - k);
+  out[i] = (uint8_t)b;
+}
+
 // host-buffer wrapper: params H2D, launches (<= 65535 poses each), outputs D2H
+// (coverage as bytes, or bit-packed per pose when `packed`)
 static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
                          int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
-                         uint8_t* coverage, int brute) {
+                         uint8_t* coverage, int brute, bool packed = false) {
   DARE_REQUIRE(n_poses >= 0, "negative pose count");
   DARE_REQUIRE(width > 0 && height > 0, "reslice plane must have at least one pixel");
   tl_last_fallback = 0;
@@ -1129,13 +1144,15 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   cudaStream_t s = thread_stream();
   const size_t npix = (size_t)n_poses * width * height;
   // call buffers from the thread's arena (slot 1; launch scratch uses slot 0)
+  const size_t hw = (size_t)width * height, bpp = (hw + 7) / 8, nbits = (size_t)n_poses * bpp;
   const size_t total = Carve::up(sizeof(double) * 14 * n_poses) + Carve::up(2 * npix) +
-                       Carve::up(sizeof(unsigned long long));
+                       Carve::up(sizeof(unsigned long long)) + (packed ? Carve::up(nbits) : 0);
   Scratch<uint8_t> block(total > kArenaMax ? total : 0, s);
   Carve cv{total > kArenaMax ? block.ptr : (uint8_t*)thread_arena(1, total, s)};
   double* d_params = cv.take<double>((size_t)n_poses * 14);
   uint8_t* d_out = cv.take<uint8_t>(2 * npix);
   unsigned long long* d_fb = cv.take<unsigned long long>(1);
+  uint8_t* d_bits = packed ? cv.take<uint8_t>(nbits) : nullptr;
   DARE_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), s));
   DARE_CUDA(cudaMemcpyAsync(d_params, params, sizeof(double) * 14 * n_poses,
                             cudaMemcpyHostToDevice, s));
@@ -1148,7 +1165,14 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   }
   unsigned long long fb = 0;
   DARE_CUDA(cudaMemcpyAsync(pixels, d_out, npix, cudaMemcpyDeviceToHost, s));
-  DARE_CUDA(cudaMemcpyAsync(coverage, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
+  if (packed) {
+    pack_coverage_k<<<ceil_div(nbits, 256), 256, 0, s>>>(d_out + npix, (int64_t)hw, (int64_t)bpp,
+                                                        (int64_t)nbits, d_bits);
+    DARE_CUDA(cudaGetLastError());
+    DARE_CUDA(cudaMemcpyAsync(coverage, d_bits, nbits, cudaMemcpyDeviceToHost, s));
+  } else {
+    DARE_CUDA(cudaMemcpyAsync(coverage, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
+  }
   DARE_CUDA(cudaMemcpyAsync(&fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
   tl_last_fallback = (int64_t)fb;
@@ -1158,6 +1182,14 @@ extern "C" int dare_reslice(dare_volume_t vol, int32_t n_poses, const double* pa
                             int32_t width, int32_t height, const dare_reslice_cfg* cfg,
                             uint8_t* pixels, uint8_t* coverage) {
   return guard([&] { reslice_host(vol, n_poses, params, width, height, cfg, pixels, coverage, 0); });
+}
+
+extern "C" int dare_reslice_packed(dare_volume_t vol, int32_t n_poses, const double* params,
+                                   int32_t width, int32_t height, const dare_reslice_cfg* cfg,
+                                   uint8_t* pixels, uint8_t* coverage_bits) {
+  return guard([&] {
+    reslice_host(vol, n_poses, params, width, height, cfg, pixels, coverage_bits, 0, true);
+  });
 }
 
 extern "C" int dare_reslice_bruteforce(dare_volume_t vol, int32_t n_poses, const double* params,

@@ -1,0 +1,294 @@
+"""Request path of the reslice service on the device.
+
+The reference server (service.py) answers each connection's newest request
+with one `reslice` (or `reslice_trilinear`) call per request and ships
+`protocol.encode_image_payload(pixels)` + `protocol.pack_coverage(coverage)`
+(service.py:273-293, protocol.py:254-275); concurrent connections each run
+their own worker thread calling the library (service.py:241-257).
+
+Here the request path keeps the reference's validation and clamping
+(`validate_request` = service.py:295-334, same messages) and its answer
+shape, but coalesces concurrent requests -- across connections -- into one
+batched launch: `ResliceBatcher` collects whatever requests are pending,
+groups them by (raster, config), and runs each group through
+`dare_reslice_packed` (coverage bit-packed on the device, np.packbits order)
+or the trilinear batch for scalar volumes.  Per-connection "newest wins"
+superseding (service.py:144-159) is `flush_requests`.  The TCP transport and
+wire framing stay out of scope (not a data-parallel path).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import time
+import zlib
+from concurrent.futures import Future
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import InvalidArgumentError
+from .geometry import Pose, Quaternion
+from .reslice import ResliceConfig, ReslicePlane, kernel_cfg, plane_params
+from .volume import as_device_volume
+
+MAX_IMAGE_DIM = 4096        # service.py:37
+MAX_RADIUS_VOXELS = 8.0     # service.py:38
+STATUS_OK, STATUS_SUPERSEDED, STATUS_ERROR = 0, 1, 2  # protocol.py:52-54
+ENCODING_RAW8, ENCODING_ZLIB = 0, 1                   # protocol.py:56-57
+
+
+@dataclass(frozen=True)
+class ResliceRequest:
+    """Field-compatible with protocol.ResliceRequest (protocol.py:94-101);
+    reference request objects are accepted as they are (duck-typed)."""
+
+    request_id: int
+    pose: tuple          # tx ty tz qw qx qy qz
+    width: int
+    height: int
+    pixel_pitch: tuple
+    encoding: int = ENCODING_RAW8
+    config: dict | None = None
+
+
+@dataclass(frozen=True)
+class ResliceResponse:
+    """Field-compatible with protocol.ResliceResponse (protocol.py:104-115)."""
+
+    request_id: int
+    status: int
+    latency_ms: float
+    width: int = 0
+    height: int = 0
+    encoding: int = ENCODING_RAW8
+    image: bytes = b""
+    coverage: bytes = b""   # packed bits, row-major, MSB first
+    superseded_by: int = 0
+    message: str = ""
+
+
+def pack_coverage(coverage) -> bytes:
+    """protocol.py:273-274 (host twin of the device packing)."""
+    return np.packbits(np.asarray(coverage, dtype=bool), axis=None).tobytes()
+
+
+def encode_image_payload(pixels, encoding: int) -> bytes:
+    """protocol.py:254-260."""
+    raw = np.ascontiguousarray(pixels, dtype=np.uint8).tobytes()
+    if encoding == ENCODING_RAW8:
+        return raw
+    if encoding == ENCODING_ZLIB:
+        return zlib.compress(raw, level=6)
+    raise InvalidArgumentError(f"unknown image encoding {encoding}")
+
+
+def clamped_config(overrides: dict, base: ResliceConfig, voxel: float) -> ResliceConfig:
+    """service.py:318-334: per-request overrides clamped to the service's ranges."""
+    radius = float(overrides.get("interp_radius", base.interp_radius))
+    radius = min(max(radius, 0.05 * voxel), MAX_RADIUS_VOXELS * voxel)
+
+    def clamp(key, default, lo, hi):
+        return min(max(float(overrides.get(key, default)), lo), hi)
+
+    return ResliceConfig(
+        interp_radius=radius,
+        normal_threshold_deg=clamp("normal_threshold_deg", base.normal_threshold_deg, 0.1, 89.9),
+        inplane_threshold_deg=clamp("inplane_threshold_deg", base.inplane_threshold_deg, 0.1, 89.9),
+        k_normal=clamp("k_normal", base.k_normal, 0.0, 1e3),
+        k_inplane=clamp("k_inplane", base.k_inplane, 0.0, 1e3),
+        k_dist=clamp("k_dist", base.k_dist, 0.0, 1e3),
+        unassigned_value=base.unassigned_value,
+    )
+
+
+def validate_request(msg, base: ResliceConfig, voxel: float) -> tuple[ReslicePlane, ResliceConfig]:
+    """service.py:295-316 (ValueError with the reference's messages)."""
+    tx, ty, tz, qw, qx, qy, qz = msg.pose
+    norm = math.sqrt(qw * qw + qx * qx + qy * qy + qz * qz)
+    if abs(norm - 1.0) > 1e-3:
+        raise ValueError(f"pose.rotation is not a unit quaternion (norm {norm:.6f})")
+    if not all(np.isfinite(msg.pose)):
+        raise ValueError("pose contains non-finite values")
+    if not (1 <= msg.width <= MAX_IMAGE_DIM and 1 <= msg.height <= MAX_IMAGE_DIM):
+        raise ValueError(f"width/height must be 1..{MAX_IMAGE_DIM}")
+    if msg.pixel_pitch[0] <= 0 or msg.pixel_pitch[1] <= 0:
+        raise ValueError("pixel_pitch must be positive")
+    if msg.encoding not in (ENCODING_RAW8, ENCODING_ZLIB):
+        raise ValueError(f"encoding must be raw8 (0) or zlib (1), got {msg.encoding}")
+    cfg = clamped_config(msg.config, base, voxel) if msg.config else base
+    plane = ReslicePlane(pose=Pose(Quaternion(qw, qx, qy, qz).normalized(), (tx, ty, tz)),
+                         width=msg.width, height=msg.height,
+                         pixel_pitch=(msg.pixel_pitch[0], msg.pixel_pitch[1]))
+    return plane, cfg
+
+
+def reslice_packed(volume, planes, cfg=None) -> tuple[np.ndarray, np.ndarray, float]:
+    """Batched directional reslice with device-packed coverage:
+    (pixels (P,H,W) u8, coverage bits (P, ceil(H*W/8)) u8, ms)."""
+    cfg = cfg or ResliceConfig()
+    planes = list(planes)
+    if not planes:
+        raise InvalidArgumentError("at least one plane required")
+    w, h = planes[0].width, planes[0].height
+    if any(p.width != w or p.height != h for p in planes):
+        raise InvalidArgumentError("all planes of a batch must share width and height")
+    params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
+    kc = kernel_cfg(cfg)
+    t0 = time.perf_counter()
+    vol = as_device_volume(volume).device_handle()
+    pixels = np.empty((len(planes), h, w), dtype=np.uint8)
+    bits = np.empty((len(planes), (h * w + 7) // 8), dtype=np.uint8)
+    _lib.call("dare_reslice_packed", vol.raw, len(planes), _lib.ptr(params, ctypes.c_double), w, h,
+              ctypes.byref(kc), _lib.ptr(pixels, ctypes.c_uint8), _lib.ptr(bits, ctypes.c_uint8))
+    return pixels, bits, (time.perf_counter() - t0) * 1000.0
+
+
+def _is_directional(volume) -> bool:
+    return hasattr(volume, "cell_counts") or hasattr(volume, "sample_count")
+
+
+@dataclass
+class _Pending:
+    msg: object
+    plane: ReslicePlane
+    cfg: ResliceConfig
+    enqueued_at: float
+    future: Future
+
+
+class ResliceBatcher:
+    """Coalesces concurrent reslice requests into batched launches.
+
+    `submit(msg)` validates on the caller's thread (errors become STATUS_ERROR
+    responses, as process_request does) and returns a Future of the
+    ResliceResponse.  One dispatcher thread drains everything pending, groups
+    it by (width, height, config) in arrival order, and launches each group
+    (<= max_batch poses) once.  Results are the library's bit-for-bit: a
+    pose's pixels do not depend on the other poses of its launch.
+    """
+
+    def __init__(self, volume, config: ResliceConfig | None = None, *, max_batch: int = 64,
+                 directional: bool | None = None):
+        self.volume = volume
+        self.config = config or ResliceConfig()
+        self.max_batch = int(max_batch)
+        if self.max_batch < 1:
+            raise InvalidArgumentError("max_batch must be >= 1")
+        self.directional = _is_directional(volume) if directional is None else bool(directional)
+        self.voxel = float(volume.voxel_size)
+        self._lock = threading.Condition()
+        self._queue: list[_Pending] = []
+        self._closed = False
+        self.launches = 0
+        self.requests = 0
+        self._thread = threading.Thread(target=self._loop, name="dare-batcher", daemon=True)
+        self._thread.start()
+
+    # -- public ---------------------------------------------------------------
+    def submit(self, msg) -> Future:
+        fut: Future = Future()
+        t0 = time.perf_counter()
+        try:
+            plane, cfg = validate_request(msg, self.config, self.voxel)
+        except Exception as e:  # answer, never raise into the connection
+            fut.set_result(_error(msg, t0, str(e)))
+            return fut
+        with self._lock:
+            if self._closed:
+                raise RuntimeError("batcher is closed")
+            self._queue.append(_Pending(msg, plane, cfg, t0, fut))
+            self._lock.notify()
+        return fut
+
+    def process_request(self, msg) -> ResliceResponse:
+        """Blocking form (service.py:273-293 signature minus the queue wrapper)."""
+        return self.submit(msg).result()
+
+    def close(self) -> None:
+        with self._lock:
+            self._closed = True
+            self._lock.notify()
+        self._thread.join()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- dispatcher -----------------------------------------------------------
+    def _loop(self):
+        while True:
+            with self._lock:
+                while not self._queue and not self._closed:
+                    self._lock.wait()
+                if not self._queue and self._closed:
+                    return
+                work, self._queue = self._queue, []
+            groups: dict = {}
+            for p in work:
+                groups.setdefault((p.plane.width, p.plane.height, p.cfg), []).append(p)
+            for (_, _, cfg), items in groups.items():
+                for i in range(0, len(items), self.max_batch):
+                    self._launch(cfg, items[i:i + self.max_batch])
+
+    def _launch(self, cfg, items):
+        planes = [p.plane for p in items]
+        try:
+            if self.directional:
+                pixels, bits, _ = reslice_packed(self.volume, planes, cfg)
+            else:
+                from .scalar import reslice_trilinear_batch
+
+                pixels, cov = reslice_trilinear_batch(self.volume, planes)[:2]
+                bits = [pack_coverage(c) for c in cov]
+            self.launches += 1
+            self.requests += len(items)
+        except Exception as e:  # noqa: BLE001 -- every request gets an answer
+            for p in items:
+                p.future.set_result(_error(p.msg, p.enqueued_at, str(e)))
+            return
+        for k, p in enumerate(items):
+            try:
+                payload = encode_image_payload(pixels[k], p.msg.encoding)
+                cov_bytes = bits[k].tobytes() if isinstance(bits, np.ndarray) else bits[k]
+                p.future.set_result(ResliceResponse(
+                    request_id=p.msg.request_id, status=STATUS_OK, latency_ms=_elapsed(p.enqueued_at),
+                    width=p.plane.width, height=p.plane.height, encoding=p.msg.encoding,
+                    image=payload, coverage=cov_bytes))
+            except Exception as e:  # noqa: BLE001
+                p.future.set_result(_error(p.msg, p.enqueued_at, str(e)))
+
+
+def flush_requests(pending: list, batcher: ResliceBatcher, enqueued_at: list[float] | None = None):
+    """service.py:144-159 for one connection: every request but the newest is
+    answered SUPERSEDED (superseded_by = newest id); the newest is resliced."""
+    if not pending:
+        return []
+    now = time.perf_counter()
+    t = enqueued_at or [now] * len(pending)
+    newest = pending[-1]
+    out = [ResliceResponse(request_id=q.request_id, status=STATUS_SUPERSEDED, latency_ms=_elapsed(t[i]),
+                           superseded_by=newest.request_id) for i, q in enumerate(pending[:-1])]
+    out.append(batcher.process_request(newest))
+    return out
+
+
+def _elapsed(t0: float) -> float:
+    return max(1e-3, (time.perf_counter() - t0) * 1000.0)
+
+
+def _error(msg, t0: float, message: str) -> ResliceResponse:
+    return ResliceResponse(request_id=getattr(msg, "request_id", 0), status=STATUS_ERROR,
+                           latency_ms=_elapsed(t0), message=message)
+
+
+__all__ = [
+    "MAX_IMAGE_DIM", "MAX_RADIUS_VOXELS", "STATUS_OK", "STATUS_SUPERSEDED", "STATUS_ERROR",
+    "ENCODING_RAW8", "ENCODING_ZLIB", "ResliceRequest", "ResliceResponse", "ResliceBatcher",
+    "pack_coverage", "encode_image_payload", "clamped_config", "validate_request",
+    "reslice_packed", "flush_requests",
+]
