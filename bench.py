@@ -331,6 +331,42 @@ def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
     }
 
 
+def service_bench(vol, planes, cfg, clients: int = 8):
+    """Requests (pose7, raster, raw8) from `clients` threads through
+    service.ResliceBatcher: wire-ready responses (pixels + device-packed
+    coverage), coalesced across clients into batched launches."""
+    import threading
+
+    from paper_2605_26325_b200 import service as svc
+
+    reqs = []
+    for i, p in enumerate(planes):
+        r = p.pose.rotation
+        reqs.append(svc.ResliceRequest(i, (*(float(c) for c in p.pose.translation), r.w, r.x, r.y, r.z),
+                                       p.width, p.height, tuple(p.pixel_pitch)))
+    with svc.ResliceBatcher(vol, cfg, max_batch=64) as b:
+        for f in [b.submit(r) for r in reqs[:16]]:
+            f.result()  # warm-up
+        b.launches = b.requests = 0
+        lat = []
+
+        def client(chunk):
+            for r in chunk:  # each client waits for its answer before the next request
+                lat.append(b.submit(r).result().latency_ms)
+
+        threads = [threading.Thread(target=client, args=(reqs[j::clients],)) for j in range(clients)]
+        t0 = time.perf_counter()
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        wall = time.perf_counter() - t0
+        return {"requests_per_s": len(reqs) / wall, "clients": clients, "requests": len(reqs),
+                "launches": b.launches, "p50_latency_ms": float(np.percentile(lat, 50)),
+                "note": "service.ResliceBatcher: validation, batched dare_reslice_packed, raw8 payload + "
+                        "packed coverage per response; each client sends its next request after the answer"}
+
+
 def host_sweep(wl, frames_np):
     from types import SimpleNamespace
 
@@ -545,6 +581,11 @@ def run_b200(args):
         lat.append(db.reslice(vol, p, cfg).timing_ms)
     p50, p95 = float(np.percentile(lat, 50)), float(np.percentile(lat, 95))
 
+    # ---- service request path: concurrent clients through ResliceBatcher ----
+    service = None
+    if rank == 0:
+        service = service_bench(vol, planes[: 8 * 32], cfg)
+
     # ---- roofline of reslice_k ----
     offsets = torch.as_tensor(DevArray(info.d_cell_offsets, (int(np.prod(info.dims)) + 1,), "<i4"), device="cuda")
     counts = (offsets[1:].long() - offsets[:-1].long())
@@ -623,7 +664,7 @@ def run_b200(args):
             "certified": certified,
             "clocks": clk,
             "cpu_baseline": cpu,
-            "scalar_arm": scalar_arm,
+            "scalar_arm": scalar_arm, "service": service,
         }
         print(json.dumps(out))
     if dist is not None:
