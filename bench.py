@@ -608,9 +608,10 @@ def run_b200(args):
         gmode = 2 if n_or == 1 else (1 if schedule == 1 and n_or <= 1024 else 0)  # register / smem / global gate
         main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}, false>"
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
-    # launches per step: gate_k, [pose_key_k + CUB single-tile sort when pixel-major], main kernel,
-    # [fallback kernel on the certified path]
-    launches_per_step = 2 + (2 if schedule == 1 and B >= 4 else 0) + (0 if args.exact else 1)
+    # launches per step: prep_k (gate table + launch order; gate_k alone when not sorted), main
+    # kernel, [fallback kernel on the certified path]
+    launches_per_step = (1 if (schedule == 1 and B >= 4) or int(info.n_orientations) > 0 else 0) + 1 + \
+        (0 if args.exact else 1)
     achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
 
     # ---- direction-blind arm (config 5): compound -> fill_holes -> trilinear ----

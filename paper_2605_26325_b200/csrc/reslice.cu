@@ -88,12 +88,9 @@ struct ResliceArgs {
 
 // gate table: one thread per (orientation, pose); the certified path's f32
 // copy is pre-scaled to log2 units.
-__global__ void gate_k(const float4* __restrict__ orient, int64_t n_orient,
-                       const double* __restrict__ params, int P, dare_reslice_cfg cfg,
-                       double* gate, float* gate2) {
-  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int p = blockIdx.y;
-  if (o >= n_orient || p >= P) return;
+__device__ __forceinline__ void gate_one(const float4* __restrict__ orient, int64_t n_orient,
+                                         const double* __restrict__ params, int64_t o, int p,
+                                         const dare_reslice_cfg& cfg, double* gate, float* gate2) {
   const double* pp = params + (size_t)p * 14;
   const double xrx = pp[3], xry = pp[6], xrz = pp[9];   // R[:,0]
   const double nrx = pp[5], nry = pp[8], nrz = pp[11];  // R[:,2]
@@ -113,6 +110,15 @@ __global__ void gate_k(const float4* __restrict__ orient, int64_t n_orient,
   }
   gate[(size_t)p * n_orient + o] = A;
   gate2[(size_t)p * n_orient + o] = __double2float_rn(A * kLog2e);
+}
+
+__global__ void gate_k(const float4* __restrict__ orient, int64_t n_orient,
+                       const double* __restrict__ params, int P, dare_reslice_cfg cfg,
+                       double* gate, float* gate2) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int p = blockIdx.y;
+  if (o >= n_orient || p >= P) return;
+  gate_one(orient, n_orient, params, o, p, cfg, gate, gate2);
 }
 
 __device__ __forceinline__ void cell_range(double w, double r, double o, double inv_v, int64_t n,
@@ -483,7 +489,8 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
                                           const float (&wl)[3], float c2, float& bw, float& bj) {
   const float g = kGate == kGateSingle ? g_single
                                        : (kGate == kGateSmem ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8)));
-  const bool k = valid && w.in_cube(c) && g != CUDART_INF_F;
+  // (single orientation: a gated-out pose never walks, see reslice_fast_k)
+  const bool k = valid && w.in_cube(c) && (kGate == kGateSingle || g != CUDART_INF_F);
   float arg = g;
   if (kDistMode != 2) {
     // (x, y) as one f32x2 lane pair (FADD2 / FMUL2); same roundings as scalar
@@ -498,7 +505,9 @@ __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const Fast
   }
   const float wt = k ? ex2_approx(arg) : 0.0f;
   // intensity as f32 without I2F: bits 2^23 + I, minus 2^23 (exact)
-  const float inten = __fsub_rn(__uint_as_float((c.w & 0xffu) | 0x4B000000u), 8388608.0f);
+  // (single orientation: every record's id is 0, the word is the intensity)
+  const uint32_t ib = kGate == kGateSingle ? c.w : (c.w & 0xffu);
+  const float inten = __fsub_rn(__uint_as_float(ib | 0x4B000000u), 8388608.0f);
   bw = __fadd_rn(bw, wt);
   bj = __fmaf_rn(wt, inten, bj);
 }
@@ -634,6 +643,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     w.s = w.e = 0;
   }
   uint32_t visits = 0;
+  // single orientation gated out for this pose: no survivor anywhere (W = 0,
+  // the pixel is certified uncovered without walking)
+  if (kGate == kGateSingle && g_single == CUDART_INF_F) live = false;
   if (live) live = w.open(a, visits, pmask);
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
@@ -832,6 +844,50 @@ __global__ void pose_key_k(const double* __restrict__ params, int P, int W, int 
   idx[p] = p;
 }
 
+// Gate table + batch launch order in ONE launch (batches of <= kRankSortMax
+// poses): blocks y < P are gate_k's; block (0, P) computes every pose's
+// pose_key_k key into shared memory and ranks them -- rank(i) = #{j : (key_j, j)
+// < (key_i, i)}, the stable order CUB's radix sort gives -- so order[rank(i)] = i.
+constexpr int kRankSortMax = 4096;
+
+__global__ void prep_k(const float4* __restrict__ orient, int64_t n_orient,
+                       const double* __restrict__ params, int P, dare_reslice_cfg cfg, double* gate,
+                       float* gate2, int W, int H, double ox, double oy, double oz, double cell,
+                       int* order) {
+  extern __shared__ unsigned long long s_keys[];
+  const int p = blockIdx.y;
+  if (p < P) {
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < n_orient) gate_one(orient, n_orient, params, o, p, cfg, gate, gate2);
+    return;
+  }
+  if (blockIdx.x != 0) return;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const double* pp = params + (size_t)i * 14;
+    const double hu = 0.5 * (W - 1) * pp[12], hv = 0.5 * (H - 1) * pp[13];
+    const double c[3] = {pp[0] + hu * pp[3] + hv * pp[4], pp[1] + hu * pp[6] + hv * pp[7],
+                         pp[2] + hu * pp[9] + hv * pp[10]};
+    const double o[3] = {ox, oy, oz};
+    unsigned long long q[3];
+    for (int k = 0; k < 3; ++k) {
+      double f = floor((c[k] - o[k]) / cell);
+      f = f < 0.0 ? 0.0 : (f > 1048575.0 ? 1048575.0 : (f != f ? 0.0 : f));
+      q[k] = (unsigned long long)f;
+    }
+    s_keys[i] = (q[2] << 40) | (q[1] << 20) | q[0];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const unsigned long long ki = s_keys[i];
+    int rank = 0;
+    for (int j = 0; j < P; ++j) {
+      const unsigned long long kj = s_keys[j];
+      rank += (kj < ki) || (kj == ki && j < i);
+    }
+    order[rank] = i;
+  }
+}
+
 __global__ void exp_k(const double* x, double* y, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = dare_exp(x[i]);
@@ -998,15 +1054,23 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   uint8_t* tmp = cv.take<uint8_t>(sort_bytes);
   a.amb = cv.take<unsigned long long>(a.amb_cap);
   a.amb_count = cv.take<unsigned>(1);
-  if (vol->n_orient > 0) {
+  a.order = nullptr;
+  const bool rank_sort = sorted && P <= kRankSortMax;
+  if (rank_sort) {  // gate table and launch order in one launch
+    prep_k<<<dim3(std::max<unsigned>(1u, ceil_div(vol->n_orient, 256)), P + 1), 256,
+             sizeof(unsigned long long) * P, s>>>(vol->d_orient, vol->n_orient, d_params, P, *cfg,
+                                                  (double*)a.gate, (float*)a.gate2, W, H, a.origin[0],
+                                                  a.origin[1], a.origin[2], 8.0 * a.voxel, order);
+    DARE_CUDA(cudaGetLastError());
+    a.order = order;
+  } else if (vol->n_orient > 0) {
     gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient,
                                                                  d_params, P, *cfg, (double*)a.gate,
                                                                  (float*)a.gate2);
     DARE_CUDA(cudaGetLastError());
   }
   pt.mark("gate");
-  a.order = nullptr;
-  if (sorted) {
+  if (sorted && !rank_sort) {
     pose_key_k<<<ceil_div(P, 128), 128, 0, s>>>(d_params, P, W, H, a.origin[0], a.origin[1],
                                                  a.origin[2], 8.0 * a.voxel, keys, idx);
     DARE_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys, keys + P, idx, order, P, 0, 60, s));
