@@ -117,15 +117,20 @@ __device__ __forceinline__ void warp_scatter(bool kept, int32_t lin, unsigned lo
 // Frames.  Thread = one pixel (u, v) over a chunk of kRunFrames consecutive
 // synchronized frames; warp = an 8(u) x 4(v) patch, block = 16 x 16 pixels.
 // Consecutive frames of a sweep put a pixel into the same cell for several
-// frames, so each thread keeps a run (cell, first frame, length <= kMaxRun,
-// the run's intensities) and only flushes when the cell changes.  Count pass:
-// one u32 reduction per run.  Fill pass: the flush is warp-aggregated over
-// lanes flushing the same cell (image neighbours): one atomic per group, ranks
-// inside the group from a bit-sliced ballot prefix of the run lengths; slot =
-// cell offset + returned cursor + rank, keys written for every sample of the run.  (Slot
-// order inside a cell is irrelevant: seal sorts every run by insertion key.)
+// frames, so each thread keeps a run (cell, first frame, length <= kMaxRun)
+// and only emits it when the cell changes.
+//   count pass (frame_count_k): the FP64 pixel -> world -> f32 -> cell chain,
+//     one u32 reduction per run into the cell histogram, and the run itself
+//     stored as an 8 B record (cell | first frame, length, z-quarter bins of
+//     its samples) in a lane-interleaved per-thread list;
+//   fill pass (frame_fill_k): no FP64 -- each thread replays its run list;
+//     lanes emitting runs of the same cell (image neighbours) are grouped with
+//     MATCH, one returning atomic per group, slots = cell offset + cursor +
+//     rank; the 64-bit key (insertion index, z bin, intensity read from the
+//     frame) is written for every sample.  Slot order inside a cell is
+//     irrelevant: the seal sorts every run by insertion key.
 constexpr int kRunFrames = 64;
-constexpr int kMaxRun = 8;  // intensities buffered in two u32
+constexpr int kMaxRun = 8;  // bins of a run's samples fit 16 bits
 
 // Sort keys: insertion index << kKeyShift | z bin << 8 | low byte (intensity for
 // frames).  The z bin (z quarter of the cell, volume.cuh) rides in bits 8-9 so
@@ -151,111 +156,137 @@ __device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, doub
   return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
 }
 
-template <bool kFill>
-__device__ __forceinline__ void run_flush(bool need, int32_t lin, uint32_t k, uint32_t run_f,
-                                          uint32_t ib0, uint32_t ib1, uint32_t bb, uint32_t pk,
-                                          uint32_t fstride,
-                                          uint32_t* counts, const uint32_t* __restrict__ offsets,
-                                          unsigned long long* keys) {
-  const unsigned lane = lane_id();
-  if (!kFill) {  // count pass: plain reductions (measured faster than the MATCH grouping)
-    if (need) atomicAdd(&counts[lin], k);
-    return;
-  }
-  // lanes not flushing get a key no cell has, so MATCH runs on the full warp
-  const unsigned peers = __match_any_sync(0xffffffffu, need ? (unsigned)lin : (0x80000000u | lane));
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned total = 0, prefix = 0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {  // k <= kMaxRun < 16
-    const unsigned mb = __ballot_sync(0xffffffffu, need && ((k >> b) & 1u)) & peers;
-    total += (unsigned)__popc(mb) << b;
-    prefix += (unsigned)__popc(mb & lt) << b;
-  }
-  // Groups whose runs cover the same frames (the common case: image neighbours
-  // crossing a cell together) take their slots frame-major -- (frame, pixel)
-  // = insertion order -- so the seal's per-cell sort finds them presorted.
-  const unsigned leader = __ffs(peers) - 1;
-  const uint32_t fk = (run_f << 4) | k;
-  const uint32_t leader_fk = __shfl_sync(0xffffffffu, fk, leader);  // all lanes (full mask)
-  const bool differs = need && leader_fk != fk;
-  const bool uniform = (__ballot_sync(0xffffffffu, differs) & peers) == 0u;
-  unsigned base = 0;
-  if (need && lane == leader) base = atomicAdd(&counts[lin], total);
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (need) {  // the group's runs take consecutive slots: coalesced key stores
-    const unsigned n = __popc(peers), rank = __popc(peers & lt);
-    unsigned long long* dst = keys + offsets[lin] + base + (uniform ? rank : prefix);
-    const uint32_t stride = uniform ? n : 1u;
-    for (uint32_t t = 0; t < k; ++t) {
-      const uint32_t inten = ((t < 4 ? ib0 : ib1) >> (8 * (t & 3))) & 0xffu;
-      dst[t * stride] = ((unsigned long long)((run_f + t) * fstride + pk) << kKeyShift) |
-                        (((bb >> (2 * t)) & 3u) << 8) | inten;
-    }
-  }
-}
-
-template <bool kFill, bool kInv>
-__global__ void __launch_bounds__(256, 5) frame_run_k(FrameView fv, uint32_t f_begin, uint32_t f_end,
-                                                   VoxelMap m, uint32_t* counts,
-                                                   const uint32_t* __restrict__ offsets,
-                                                   unsigned long long* keys,
-                                                   unsigned long long* rejected) {
-  __shared__ double s_axes[kRunFrames * 9];
-  __shared__ uint32_t s_img[kRunFrames];
+// thread -> pixel of a 16 x 16 tile (warp = 8 x 4), shared by both passes
+__device__ __forceinline__ void tile_pixel(const FrameView& fv, uint32_t& u, uint32_t& v) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t tiles_u = (fv.W + 15) / 16;
-  const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
-  const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const uint32_t p = v * fv.W + u, pk = fv.pixel_key(u, v);
+  u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
+  v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
+}
+
+// Run record: x = cell, y = first frame in the chunk (6 bits) | length << 6 |
+// z bins (2 bits per sample) << 10.  Lane-interleaved: run r of thread t of
+// block b at runs[(b * kRunFrames + r) * 256 + t].
+template <bool kInv>
+__global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m, uint32_t* counts,
+                                                      uint2* __restrict__ runs, uint8_t* __restrict__ nruns,
+                                                      unsigned long long* rejected) {
+  __shared__ double s_axes[kRunFrames * 9];
+  uint32_t u, v;
+  tile_pixel(fv, u, v);
+  const uint32_t lane = lane_id();
+  const uint32_t p = v * fv.W + u;
   const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
-  const uint32_t f0 = f_begin + blockIdx.y * kRunFrames;
-  const int nf = (int)min((uint32_t)kRunFrames, f_end - f0);
+  const uint32_t f0 = blockIdx.y * kRunFrames;
+  const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
   for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[(size_t)f0 * 9 + i];
-  if (kFill)
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (uint32_t)fv.image[f0 + i];
   __syncthreads();
+  const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+  uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   int32_t cur = -1;
-  uint32_t run_f = 0, k = 0, ib0 = 0, ib1 = 0, bb = 0;
-  float zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;  // z-quarter bounds of the run's cell (fill)
-  // intensities loaded one frame ahead (latency hidden behind the frame's math)
-  uint32_t inten_next = (kFill && in_frame && nf > 0) ? fv.frames[(size_t)s_img[0] * fv.hw + p] : 0u;
+  uint32_t run_j = 0, k = 0, bb = 0, nr = 0;
+  float zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;  // z-quarter bounds of the run's cell
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count
-    const uint32_t inten = inten_next;
-    if (kFill && in_frame && j + 1 < nf) inten_next = fv.frames[(size_t)s_img[j + 1] * fv.hw + p];
     float z = 0.f;
     uint32_t iz = 0;
     const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m, z, iz) : -1;
-    if (!kFill) {
-      const unsigned oob = __ballot_sync(0xffffffffu, in_frame && lin < 0);
-      if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
-    }
+    const unsigned oob = __ballot_sync(0xffffffffu, in_frame && lin < 0);
+    if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
-    const bool need = restart && cur >= 0;
-    if (__any_sync(0xffffffffu, need))
-      run_flush<kFill>(need, cur, k, run_f, ib0, ib1, bb, pk, fv.fstride, counts, offsets, keys);
+    if (restart && cur >= 0) {
+      atomicAdd(&counts[cur], k);
+      my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
+      ++nr;
+    }
     if (restart) {
       cur = lin;
-      run_f = f0 + j;
+      run_j = (uint32_t)j;
       k = 0;
-      ib0 = ib1 = bb = 0;
-      if (kFill && lin >= 0) {
+      bb = 0;
+      if (lin >= 0) {
         zb1 = zbin_bound(m.origin[2], m.voxel, iz, 1);
         zb2 = zbin_bound(m.origin[2], m.voxel, iz, 2);
         zb3 = zbin_bound(m.origin[2], m.voxel, iz, 3);
       }
     }
-    if (kFill && lin >= 0) {
-      bb |= (uint32_t)((z >= zb1) + (z >= zb2) + (z >= zb3)) << (2 * k);
-      if (k < 4) ib0 |= inten << (8 * k);
-      else ib1 |= inten << (8 * (k - 4));
-    }
+    if (lin >= 0) bb |= (uint32_t)((z >= zb1) + (z >= zb2) + (z >= zb3)) << (2 * k);
     ++k;
   }
-  const bool need = cur >= 0;
-  if (__any_sync(0xffffffffu, need))
-    run_flush<kFill>(need, cur, k, run_f, ib0, ib1, bb, pk, fv.fstride, counts, offsets, keys);
+  if (cur >= 0) {
+    atomicAdd(&counts[cur], k);
+    my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
+    ++nr;
+  }
+  nruns[blk * 256 + threadIdx.x] = (uint8_t)nr;  // <= kRunFrames
+}
+
+// Fill pass over the chunks [chunk_begin, chunk_begin + gridDim.y): replays
+// each thread's runs (see frame_count_k); no pixel geometry is recomputed.
+__global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk_begin,
+                                                    const uint2* __restrict__ runs,
+                                                    const uint8_t* __restrict__ nruns, uint32_t* counts,
+                                                    const uint32_t* __restrict__ offsets,
+                                                    unsigned long long* keys) {
+  __shared__ uint32_t s_img[kRunFrames];
+  uint32_t u, v;
+  tile_pixel(fv, u, v);
+  const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
+  const uint32_t p = v * fv.W + u, pk = fv.pixel_key(u, v);
+  const uint32_t chunk = chunk_begin + blockIdx.y, f0 = chunk * kRunFrames;
+  const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (uint32_t)fv.image[f0 + i];
+  __syncthreads();
+  const size_t blk = (size_t)chunk * gridDim.x + blockIdx.x;
+  const uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
+  const uint32_t nr = nruns[blk * 256 + threadIdx.x];
+  const uint32_t max_nr = __reduce_max_sync(0xffffffffu, nr);
+  uint2 next = nr > 0 ? my[0] : make_uint2(0u, 0u);
+  for (uint32_t r = 0; r < max_nr; ++r) {
+    const bool need = r < nr;
+    const uint2 run = next;
+    if (r + 1 < nr) next = my[(size_t)(r + 1) * 256];  // one run ahead
+    const uint32_t lin = run.x, run_j = run.y & 63u, k = (run.y >> 6) & 15u, bb = run.y >> 10;
+    // intensities first: their latency overlaps the grouping and the atomic
+    uint32_t inten[kMaxRun];
+#pragma unroll
+    for (int t = 0; t < kMaxRun; ++t)
+      inten[t] = (need && (uint32_t)t < k) ? fv.frames[(size_t)s_img[run_j + t] * fv.hw + p] : 0u;
+    // lanes not emitting get a key no cell has, so MATCH runs on the full warp
+    const unsigned peers = __match_any_sync(0xffffffffu, need ? lin : (0x80000000u | lane));
+    unsigned total = 0, prefix = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {  // k <= kMaxRun < 16
+      const unsigned mb = __ballot_sync(0xffffffffu, need && ((k >> b) & 1u)) & peers;
+      total += (unsigned)__popc(mb) << b;
+      prefix += (unsigned)__popc(mb & lt) << b;
+    }
+    // Groups whose runs cover the same frames (the common case: image
+    // neighbours crossing a cell together) take their slots frame-major --
+    // (frame, pixel) = insertion order -- so the seal's sort finds them presorted.
+    const unsigned leader = __ffs(peers) - 1;
+    const uint32_t fk = (run_j << 4) | k;
+    const uint32_t leader_fk = __shfl_sync(0xffffffffu, fk, leader);  // all lanes (full mask)
+    const bool differs = need && leader_fk != fk;
+    const bool uniform = (__ballot_sync(0xffffffffu, differs) & peers) == 0u;
+    unsigned base = 0;
+    if (need && lane == leader) base = atomicAdd(&counts[lin], total);
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (need) {
+      const unsigned n = __popc(peers), rank = __popc(peers & lt);
+      const uint32_t stride = uniform ? n : 1u;
+      unsigned long long* dst = keys + offsets[lin] + base + (uniform ? rank : prefix);
+      const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
+      const unsigned long long kstep = (unsigned long long)fv.fstride << kKeyShift;
+#pragma unroll
+      for (int t = 0; t < kMaxRun; ++t) {
+        if ((uint32_t)t < k) {
+          *dst = key0 + (unsigned long long)t * kstep + (((bb >> (2 * t)) & 3u) << 8) + inten[t];
+          dst += stride;
+        }
+      }
+    }
+  }
 }
 
 // Arbitrary samples (VolumeBuilder.seal, volume.py:240-269): key = sample index
@@ -705,26 +736,27 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                                 cudaMemcpyHostToDevice, s));
     }
     DARE_LIMIT(ceil_div(n_frames, kRunFrames) <= 65535, "too many frames for one launch");
+    const unsigned tiles = ceil_div(width, 16) * ceil_div(height, 16);
+    const unsigned chunks = ceil_div(std::max<int64_t>(n_frames, 1), kRunFrames);
+    // per-thread run lists of the count pass (8 B per run, <= one run per frame)
+    Scratch<uint2> runs(n_frames > 0 ? (size_t)tiles * chunks * kRunFrames * 256 : 0, s);
+    Scratch<uint8_t> nruns(n_frames > 0 ? (size_t)tiles * chunks * 256 : 0, s);
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
                        unsigned long long* keys, unsigned long long* rej) {
       if (n_frames == 0) return;
-      const unsigned tiles = ceil_div(width, 16) * ceil_div(height, 16);
       if (!fill) {  // needs no intensities: runs while host frames are still uploading
-        (m.exact_inv ? frame_run_k<false, true> : frame_run_k<false, false>)<<<
-            dim3(tiles, (unsigned)ceil_div(n_frames, kRunFrames)), 256, 0, s>>>(
-            fv, 0u, (uint32_t)n_frames, m, counts, offsets, keys, rej);
+        (m.exact_inv ? frame_count_k<true> : frame_count_k<false>)<<<dim3(tiles, chunks), 256, 0, s>>>(
+            fv, m, counts, runs.ptr, nruns.ptr, rej);
         return;
       }
-      // fill in groups of frames, each launched once its images are resident
+      // fill in groups of chunks, each launched once its images are resident
       // (one launch per upload group, so fill overlaps the rest of the transfer)
-      const int64_t step = fs.done.empty() ? n_frames
-                                           : std::max<int64_t>(kRunFrames, ceil_div(fs.per_group, kRunFrames) * kRunFrames);
-      for (int64_t f0 = 0; f0 < n_frames; f0 += step) {
-        const int64_t f1 = std::min<int64_t>(n_frames, f0 + step);
-        fs.wait_frames(s, f0, f1);
-        (m.exact_inv ? frame_run_k<true, true> : frame_run_k<true, false>)<<<
-            dim3(tiles, (unsigned)ceil_div(f1 - f0, kRunFrames)), 256, 0, s>>>(
-            fv, (uint32_t)f0, (uint32_t)f1, m, counts, offsets, keys, rej);
+      const int64_t step = fs.done.empty() ? chunks : std::max<int64_t>(1, ceil_div(fs.per_group, kRunFrames));
+      for (int64_t c0 = 0; c0 < (int64_t)chunks; c0 += step) {
+        const int64_t c1 = std::min<int64_t>(chunks, c0 + step);
+        fs.wait_frames(s, c0 * kRunFrames, std::min<int64_t>(n_frames, c1 * kRunFrames));
+        frame_fill_k<<<dim3(tiles, (unsigned)(c1 - c0)), 256, 0, s>>>(fv, (uint32_t)c0, runs.ptr, nruns.ptr,
+                                                                      counts, offsets, keys);
       }
     };
     Scratch<SealAxes> sa((size_t)std::max<int64_t>(n_frames, 1), s);
