@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
 #pragma unroll
     for (int t = 0; t < kMaxRun; ++t)
       inten[t] = (need && (uint32_t)t < k) ? fv.frames[(size_t)s_img[run_j + t] * fv.hw + p] : 0u;
+    const uint32_t cell_off = need ? offsets[lin] : 0u;  // issued early: overlaps the atomic
     // lanes not emitting get a key no cell has, so MATCH runs on the full warp
     const unsigned peers = __match_any_sync(0xffffffffu, need ? lin : (0x80000000u | lane));
     unsigned total = 0, prefix = 0;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
       const uint32_t stride = uniform ? n : 1u;
-      unsigned long long* dst = keys + offsets[lin] + base + (uniform ? rank : prefix);
+      unsigned long long* dst = keys + cell_off + base + (uniform ? rank : prefix);
       const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
       const unsigned long long kstep = (unsigned long long)fv.fstride << kKeyShift;
 #pragma unroll
