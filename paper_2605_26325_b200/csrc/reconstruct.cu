@@ -23,6 +23,7 @@
 //              segmented sort and are (re)written afterwards.
 // All pixel/cell index math is 32-bit (dims < 2^31 cells, < 2^32 pixels) with
 // a multiply-high divider, which keeps the per-pixel instruction count low.
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
@@ -408,16 +409,19 @@ struct SampleRecords {
   __device__ __forceinline__ float z_of(uint32_t pid) const { return pos[3 * (size_t)pid + 2]; }
 };
 
-constexpr int kSmallRun = 32;  // per-cell runs sorted in shared memory by one lane
+constexpr int kSmallRun = 32;  // longest per-cell run sorted in shared memory by one lane
 constexpr int kSealWarps = 4;  // warps per seal block
 constexpr int kPitch = 33;     // odd row pitch: both access patterns conflict-free
 
+// kRun = the longest run the stage holds (16 or 32): the host picks 16 when no
+// cell has more samples (half the shared memory: 10 instead of 7 blocks/SM)
+template <int kRun>
 struct SealSmem {
-  uint32_t st[kSmallRun * kPitch];  // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
-  uint16_t sx[kSmallRun * kPitch];  // its low key byte | z bin << 8, later | destination << 8
-  uint16_t cstart[32];              // cell start relative to the warp's first key
-  uint8_t cell_of[kSmallRun * 32];  // key position -> lane of its cell
-  float zb[3][32];                  // z-quarter boundaries of each lane's cell (SampleRecords)
+  uint32_t st[kRun * kPitch];  // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
+  uint16_t sx[kRun * kPitch];  // its low key byte | z bin << 8, later | destination << 8
+  uint16_t cstart[32];         // cell start relative to the warp's first key
+  uint8_t cell_of[kRun * 32];  // key position -> lane of its cell
+  float zb[3][32];             // z-quarter boundaries of each lane's cell (SampleRecords)
 };
 
 // z-quarter binning of the sealed runs (layout in volume.cuh)
@@ -437,16 +441,16 @@ struct BinOut {
 // are written back coalesced with perm.  Runs longer than kSmallRun are listed
 // for the CUB segmented-sort path; they, and the small runs of a warp that
 // has one, stay in insertion order (bins 0, perm 0).
-template <class Rec>
-__global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
+template <class Rec, int kRun>
+__global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(Rec rec,
                                                           const uint32_t* __restrict__ offsets,
                                                           const unsigned long long* __restrict__ keys,
                                                           uint32_t ncells, uint4* records,
                                                           uint32_t* big_cells, uint32_t* n_big,
                                                           BinOut bo) {
-  __shared__ SealSmem smem[kSealWarps];
+  __shared__ SealSmem<kRun> smem[kSealWarps];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  SealSmem& sm = smem[warp];
+  SealSmem<kRun>& sm = smem[warp];
   // warp -> 32 consecutive cells of one column, z-chunk-major across warps:
   // concurrently resident warps cover the same z range of many columns, so a
   // z sweep's records come from the same few frames (L1-resident axes)
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
     cs = offsets[c];
     cn = offsets[c + 1] - cs;
   }
-  const bool big = cn > kSmallRun;
+  const bool big = cn > kRun;
   if (big) big_cells[atomicAdd(n_big, 1u)] = c;
   const uint32_t len = s1 - s0;
   const bool staged = !__any_sync(0xffffffffu, big);  // then len <= 32 * 32
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(kSealWarps * 32) seal_k(Rec rec,
     }
   } else if (cn > 0 && !big) {
     // a big run in this warp's chunk: the small runs are sealed lane by lane
-    unsigned long long k[kSmallRun];
+    unsigned long long k[kRun];
     for (uint32_t i = 0; i < cn; ++i) {
       const unsigned long long x = keys[cs + i];
       uint32_t j = i;
@@ -604,17 +608,21 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   scatter(false, counts.ptr, (const uint32_t*)nullptr, (unsigned long long*)nullptr, rej.ptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
-  size_t tmp_bytes = 0;
+  size_t tmp_bytes = 0, max_bytes = 0;
+  Scratch<uint32_t> max_d(1, s);
   DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.ptr, vol->d_offsets,
                                           ncells + 1, s));
+  DARE_CUDA(cub::DeviceReduce::Max(nullptr, max_bytes, counts.ptr, max_d.ptr, ncells, s));
   {
-    Scratch<uint8_t> tmp(tmp_bytes, s);
+    Scratch<uint8_t> tmp(std::max(tmp_bytes, max_bytes), s);
     DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, counts.ptr, vol->d_offsets,
                                             ncells + 1, s));
+    DARE_CUDA(cub::DeviceReduce::Max(tmp.ptr, max_bytes, counts.ptr, max_d.ptr, ncells, s));
   }
   pt.mark("scan");
-  uint32_t n_kept = 0;
+  uint32_t n_kept = 0, max_run = 0;
   unsigned long long n_rej = 0;
+  DARE_CUDA(cudaMemcpyAsync(&max_run, max_d.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaMemcpyAsync(&n_kept, vol->d_offsets + ncells, sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaMemcpyAsync(&n_rej, rej.ptr, sizeof(n_rej), cudaMemcpyDeviceToHost, s));
@@ -644,10 +652,12 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     // L1 misses, so trade shared-memory carve-out (occupancy) for L1
     const char* e = getenv("DARE_SEAL_CARVEOUT");  // development override
     const int carve = e ? atoi(e) : seal_carveout;
-    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault));
+    const int c = carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault;
+    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, kSmallRun>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
   }
-  seal_k<<<ceil_div((ncells / vol->dims[2]) * ceil_div(vol->dims[2], 32), kSealWarps), 32 * kSealWarps, 0, s>>>(
+  (max_run <= 16 ? seal_k<Rec, 16> : seal_k<Rec, kSmallRun>)<<<
+      ceil_div((ncells / vol->dims[2]) * ceil_div(vol->dims[2], 32), kSealWarps), 32 * kSealWarps, 0, s>>>(
       rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr,
       BinOut{vol->origin[2], vol->voxel, vol->dims[2], vol->d_bins, vol->d_perm});
   DARE_CUDA(cudaGetLastError());
