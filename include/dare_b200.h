@@ -180,6 +180,22 @@ int dare_volume_destroy(dare_volume_t vol);
 int dare_reslice(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
                  int32_t height, const dare_reslice_cfg* cfg, uint8_t* pixels,
                  uint8_t* coverage);
+/* Host-side pose pipeline (no device work) for n synchronized frames, replacing
+ * the per-frame Python of synchronize() after interpolation (reconstruct.py:119-149:
+ * marker.compose(calibration) = normalised qmul + rotate(q, t_cal) + t,
+ * geometry.py:69-77, 99-107, 128-133), the frame axes (rotation_matrix,
+ * geometry.py:79-88; reconstruct.py:155-162), the canonical f32 quaternions
+ * (reconstruct.py:192-195) and the image corners of compute_bounds
+ * (volume.py:57-73).  mq n x 4 marker quaternions (w,x,y,z), mt n x 3; cal_q[4],
+ * cal_t[3].  Outputs: rot n x 4, trans n x 3, axes n x 9 (R[:,0], R[:,1], t),
+ * quats32 n x 4, lo[3] / hi[3] = compute_bounds' corner box before the
+ * margin (sequential np.minimum / np.maximum).  *status: 0 ok, 1 zero quaternion (frame
+ * *bad), 2 marker quaternion not unit (*bad, norm *bad_norm), 3 frame rotation
+ * not unit (corners; *bad, *bad_norm) -- the caller raises the reference's error. */
+int dare_frame_poses(int64_t n, const double* mq, const double* mt, const double* cal_q,
+                     const double* cal_t, int32_t width, int32_t height, double px, double py,
+                     double* rot, double* trans, double* axes, float* quats32, double* lo,
+                     double* hi, int32_t* status, int64_t* bad, double* bad_norm);
 /* Service form of dare_reslice (service.py:273-293 process_request, which
  * reslices one request and ships protocol.pack_coverage(image.coverage),
  * protocol.py:273-274): same pixels; coverage bit-packed on the device per pose

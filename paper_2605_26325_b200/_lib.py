@@ -83,6 +83,9 @@ _SIGNATURES = {
     "dare_volume_download": [c_vp, P_i64, P_i64, P_f32, P_f32, P_u8],
     "dare_volume_get_info": [c_vp, ctypes.POINTER(VolumeInfo)],
     "dare_volume_destroy": [c_vp],
+    "dare_frame_poses": [c_i64, P_f64, P_f64, P_f64, P_f64, c_i32, c_i32, c_f64, c_f64, P_f64, P_f64, P_f64,
+                         P_f32, P_f64, P_f64, ctypes.POINTER(c_i32), ctypes.POINTER(c_i64),
+                         ctypes.POINTER(c_f64)],
     "dare_reslice": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_packed": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_bruteforce": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8,

@@ -11,6 +11,8 @@ not elementwise numpy.
 """
 from __future__ import annotations
 
+import ctypes
+import itertools
 import math
 import operator
 from dataclasses import dataclass, field
@@ -106,6 +108,12 @@ class FramePlan:
     pixel_pitch: tuple[float, float]
     height: int
     width: int
+    # from dare_frame_poses (csrc/plan.cu), same bits as the numpy restatements
+    # below; None when the plan was built from arrays directly
+    _axes: np.ndarray | None = field(default=None, repr=False)
+    _quats32: np.ndarray | None = field(default=None, repr=False)
+    _corner_box: tuple | None = field(default=None, repr=False)  # (lo, hi) before the margin
+    _corner_error: str | None = field(default=None, repr=False)
 
     @property
     def n_frames(self) -> int:
@@ -113,11 +121,15 @@ class FramePlan:
 
     def axes(self) -> np.ndarray:
         """(n, 9): R[:,0], R[:,1], t per frame (reconstruct.py:155-162)."""
+        if self._axes is not None:
+            return self._axes
         r = geo.rotation_matrices(self.rotations)
         return np.ascontiguousarray(np.concatenate([r[:, :, 0], r[:, :, 1], self.translations], axis=1))
 
     def canonical_quats_f32(self) -> np.ndarray:
         """(n, 4) f32 canonical frame quaternions (reconstruct.py:192-195)."""
+        if self._quats32 is not None:
+            return self._quats32
         q = self.rotations
         w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
         flip = (w < 0.0) | ((w == 0.0) & ((x < 0.0) | ((x == 0.0) & ((y < 0.0) | ((y == 0.0) & (z < 0.0))))))
@@ -129,19 +141,30 @@ class FramePlan:
 
         if self.n_frames == 0:
             raise InvalidArgumentError("compute_bounds requires at least one frame")
+        if self._corner_box is not None:
+            if self._corner_error is not None:
+                raise InvalidArgumentError(self._corner_error)
+            return BoundingBox(*self._corner_box).expanded(margin)
+        # numpy restatement: the same sequential np.minimum / np.maximum
         px, py = self.pixel_pitch
         umax = (self.width - 1) * px
         vmax = (self.height - 1) * py
         corners = np.array([(0.0, 0.0, 0.0), (umax, 0.0, 0.0), (0.0, vmax, 0.0), (umax, vmax, 0.0)])
-        c = geo.rotate_grid(self.rotations, corners) + self.translations[:, None, :]
-        return BoundingBox(c.min(axis=(0, 1)), c.max(axis=(0, 1))).expanded(margin)
+        c = (geo.rotate_grid(self.rotations, corners) + self.translations[:, None, :]).reshape(-1, 3)
+        lo, hi = np.full(3, np.inf), np.full(3, -np.inf)
+        for row in c:
+            lo = np.minimum(lo, row)
+            hi = np.maximum(hi, row)
+        return BoundingBox(lo, hi).expanded(margin)
 
 
 _wxyz = operator.attrgetter("w", "x", "y", "z")
+_rotation = operator.attrgetter("rotation")
 
 
 def _quat_array(poses) -> np.ndarray:
-    return np.array([_wxyz(p.rotation) for p in poses], dtype=float).reshape(-1, 4)
+    return np.fromiter(itertools.chain.from_iterable(map(_wxyz, map(_rotation, poses))), dtype=float,
+                       count=4 * len(poses)).reshape(-1, 4)
 
 
 def _translation_array(poses) -> np.ndarray:
@@ -183,7 +206,44 @@ def plan_frames(sweep) -> FramePlan:
         mq[j] = (m.rotation.w, m.rotation.x, m.rotation.y, m.rotation.z)
         mt[j] = m.translation
 
-    cal = sweep.calibration
+    return _compose_plan(kept, mq, mt, sweep.calibration, dropped, (float(px), float(py)), int(height), int(width))
+
+
+def _compose_plan(kept, mq, mt, cal, dropped, pitch, height, width) -> FramePlan:
+    """Marker pose o calibration, axes, canonical f32 quaternions and image
+    corners for every frame in one host call (csrc/plan.cu: dare_frame_poses)."""
+    from . import _lib
+
+    n = len(kept)
+    mq = np.ascontiguousarray(mq, dtype=np.float64)
+    mt = np.ascontiguousarray(mt, dtype=np.float64)
+    cq = cal.rotation
+    cal_q = np.array([cq.w, cq.x, cq.y, cq.z], dtype=np.float64)
+    cal_t = np.ascontiguousarray(np.asarray(cal.translation, dtype=float).reshape(3))
+    rot = np.empty((n, 4))
+    trans = np.empty((n, 3))
+    axes = np.empty((n, 9))
+    q32 = np.empty((n, 4), dtype=np.float32)
+    lo, hi = np.empty(3), np.empty(3)
+    status, bad, bad_norm = ctypes.c_int32(0), ctypes.c_int64(-1), ctypes.c_double(0.0)
+    P = ctypes.c_double
+    _lib.call("dare_frame_poses", n, _lib.ptr(mq, P), _lib.ptr(mt, P), _lib.ptr(cal_q, P), _lib.ptr(cal_t, P),
+              int(width), int(height), pitch[0], pitch[1], _lib.ptr(rot, P), _lib.ptr(trans, P),
+              _lib.ptr(axes, P), _lib.ptr(q32, ctypes.c_float), _lib.ptr(lo, P), _lib.ptr(hi, P), ctypes.byref(status),
+              ctypes.byref(bad), ctypes.byref(bad_norm))
+    norm_msg = "quaternion norm {:.6f} deviates from 1 by more than " + str(geo.UNIT_NORM_TOL)
+    if status.value == 1:
+        raise InvalidArgumentError("cannot normalize zero quaternion")
+    if status.value == 2:
+        raise InvalidArgumentError(norm_msg.format(bad_norm.value))
+    corner_error = norm_msg.format(bad_norm.value) if status.value == 3 else None
+    return FramePlan(kept.astype(np.int32), rot, trans, dropped, pitch, height, width,
+                     _axes=axes, _quats32=q32, _corner_box=(lo, hi), _corner_error=corner_error)
+
+
+def _compose_plan_numpy(kept, mq, mt, cal, dropped, pitch, height, width) -> FramePlan:
+    """The same composition restated in numpy (cross-check for tests)."""
+    px, py = pitch
     cq = cal.rotation
     w, x, y, z = mq[:, 0], mq[:, 1], mq[:, 2], mq[:, 3]
     prod = np.stack([

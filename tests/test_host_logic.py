@@ -147,3 +147,39 @@ def test_device_code_is_sm100a_only():
                          text=True).stdout
     archs = set(re.findall(r"sm_\d+a?", out))
     assert archs == {"sm_100a"}, archs
+
+
+def test_frame_pose_pipeline_c_equals_numpy():
+    """dare_frame_poses (csrc/plan.cu) gives the numpy restatement's bits:
+    rotations, translations, axes, canonical f32 quaternions, bounds; and the
+    reference's errors."""
+    from paper_2605_26325_b200 import sweep as S
+
+    rng = np.random.default_rng(11)
+    n = 300
+    mq = rng.normal(size=(n, 4))
+    mq /= np.linalg.norm(mq, axis=1, keepdims=True)
+    mq[::7] *= -1.0
+    mq[5] = (0.0, -0.6, 0.8, 0.0)  # w == 0: tie-broken sign
+    mt = rng.uniform(-50, 50, (n, 3))
+    cal = Pose(Quaternion.from_axis_angle((0.3, -1.0, 0.2), 0.7), (1.5, -2.25, 0.125))
+    kept = np.arange(n)
+    a = S._compose_plan(kept, mq, mt, cal, 0, (0.137, 0.211), 47, 63)
+    b = S._compose_plan_numpy(kept, mq, mt, cal, 0, (0.137, 0.211), 47, 63)
+    np.testing.assert_array_equal(a.rotations, b.rotations)
+    np.testing.assert_array_equal(a.translations, b.translations)
+    np.testing.assert_array_equal(a.axes(), b.axes())
+    np.testing.assert_array_equal(a.canonical_quats_f32(), b.canonical_quats_f32())
+    ba, bb = a.bounds(0.5), b.bounds(0.5)
+    np.testing.assert_array_equal(ba.min, bb.min)
+    np.testing.assert_array_equal(ba.max, bb.max)
+    bad = mq.copy()
+    bad[3] = 0.0
+    with pytest.raises(InvalidArgumentError, match="cannot normalize zero quaternion"):
+        S._compose_plan(kept, bad, mt, cal, 0, (0.1, 0.1), 4, 4)
+    bad = mq.copy()
+    bad[9] *= 1.01
+    with pytest.raises(InvalidArgumentError, match="quaternion norm 1.010000 deviates from 1 by more than 0.001"):
+        S._compose_plan(kept, bad, mt, cal, 0, (0.1, 0.1), 4, 4)
+    with pytest.raises(InvalidArgumentError, match="quaternion norm 1.010000 deviates"):
+        S._compose_plan_numpy(kept, bad, mt, cal, 0, (0.1, 0.1), 4, 4)
