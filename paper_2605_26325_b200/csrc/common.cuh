@@ -85,6 +85,13 @@ inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) /
 // safe and saves the per-call allocator round trips of small launches.
 void* thread_arena(int slot, size_t bytes, cudaStream_t s);
 
+// Grow-only pinned host buffer per host thread: staging for small pageable
+// host-buffer calls (latency: async copies, one synchronisation).  Contents
+// are only valid until the thread's next call.
+void* thread_pinned(size_t bytes);
+// true when `p` is page-locked (cudaMallocHost / cudaHostRegister) host memory
+bool host_pinned(const void* p);
+
 // Bump carving of one scratch block (256 B aligned pieces).
 struct Carve {
   uint8_t* base = nullptr;

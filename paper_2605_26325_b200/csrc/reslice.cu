@@ -32,6 +32,7 @@
 //     a power of two, skipped when k_d == 0; exp is the glibc port (dare_exp.h).
 #include <math_constants.h>
 
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -1196,6 +1197,8 @@ __global__ void pack_coverage_k(const uint8_t* __restrict__ cov, int64_t hw, int
   out[i] = (uint8_t)b;
 }
 
+constexpr size_t kStageMax = 4u << 20;  // outputs staged through pinned memory up to this size
+
 // host-buffer wrapper: params H2D, launches (<= 65535 poses each), outputs D2H
 // (coverage as bytes, or bit-packed per pose when `packed`)
 static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* params, int32_t width,
@@ -1218,8 +1221,18 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   unsigned long long* d_fb = cv.take<unsigned long long>(1);
   uint8_t* d_bits = packed ? cv.take<uint8_t>(nbits) : nullptr;
   DARE_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), s));
-  DARE_CUDA(cudaMemcpyAsync(d_params, params, sizeof(double) * 14 * n_poses,
-                            cudaMemcpyHostToDevice, s));
+  // small calls from pageable memory (the latency path): stage through the
+  // thread's pinned buffer -- async copies and a single synchronisation
+  const size_t out_bytes = npix + (packed ? nbits : npix);
+  const bool stage = out_bytes <= kStageMax && !host_pinned(pixels);
+  const size_t pbytes = sizeof(double) * 14 * n_poses;
+  uint8_t* h_stage = stage ? (uint8_t*)thread_pinned(pbytes + out_bytes + sizeof(unsigned long long)) : nullptr;
+  const double* h_params = params;
+  if (stage) {
+    memcpy(h_stage, params, pbytes);
+    h_params = (const double*)h_stage;
+  }
+  DARE_CUDA(cudaMemcpyAsync(d_params, h_params, pbytes, cudaMemcpyHostToDevice, s));
   for (int32_t p0 = 0; p0 < n_poses; p0 += 65535) {
     int32_t np = std::min<int32_t>(65535, n_poses - p0);
     size_t off = (size_t)p0 * width * height;
@@ -1228,17 +1241,26 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
                    poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel), d_fb);
   }
   unsigned long long fb = 0;
-  DARE_CUDA(cudaMemcpyAsync(pixels, d_out, npix, cudaMemcpyDeviceToHost, s));
+  const size_t cov_bytes = packed ? nbits : npix;
+  uint8_t* h_px = stage ? h_stage + pbytes : pixels;
+  uint8_t* h_cov = stage ? h_px + npix : coverage;
+  unsigned long long* h_fb = stage ? (unsigned long long*)(h_cov + cov_bytes) : &fb;
+  DARE_CUDA(cudaMemcpyAsync(h_px, d_out, npix, cudaMemcpyDeviceToHost, s));
   if (packed) {
     pack_coverage_k<<<ceil_div(nbits, 256), 256, 0, s>>>(d_out + npix, (int64_t)hw, (int64_t)bpp,
                                                         (int64_t)nbits, d_bits);
     DARE_CUDA(cudaGetLastError());
-    DARE_CUDA(cudaMemcpyAsync(coverage, d_bits, nbits, cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaMemcpyAsync(h_cov, d_bits, nbits, cudaMemcpyDeviceToHost, s));
   } else {
-    DARE_CUDA(cudaMemcpyAsync(coverage, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaMemcpyAsync(h_cov, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
   }
-  DARE_CUDA(cudaMemcpyAsync(&fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
+  DARE_CUDA(cudaMemcpyAsync(h_fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
+  if (stage) {
+    memcpy(pixels, h_px, npix);
+    memcpy(coverage, h_cov, cov_bytes);
+    fb = *h_fb;
+  }
   tl_last_fallback = (int64_t)fb;
 }
 

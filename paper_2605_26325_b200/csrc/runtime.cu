@@ -91,6 +91,35 @@ void* thread_arena(int slot, size_t bytes, cudaStream_t s) {
   return b.p;
 }
 
+void* thread_pinned(size_t bytes) {
+  struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~Pinned() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Pinned b;
+  if (b.cap < bytes) {
+    if (b.p) DARE_CUDA(cudaFreeHost(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+    const size_t want = std::max<size_t>(bytes, 1 << 20);
+    DARE_CUDA(cudaMallocHost(&b.p, want));
+    b.cap = want;
+  }
+  return b.p;
+}
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: plain pageable memory on older runtimes
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 void dev_free(void* p) {
   if (!p) return;
   try {
