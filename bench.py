@@ -175,7 +175,11 @@ def ncu_traffic(kernel: str, batch: int, config: str):
             data = json.load(fh)
         if config != "cfg2" or batch != 64:
             return None, "ncu capture is for cfg2 / 64 poses per launch"
-        return float(data["dram_bytes_per_launch"][kernel]), "profiles/round1_traffic.json (" + data["source"] + ")"
+        table = data["dram_bytes_per_launch"]
+        # ncu prints bool template arguments as 0/1
+        alt = kernel.replace("false", "0").replace("true", "1")
+        key = kernel if kernel in table else alt
+        return float(table[key]), "profiles/round1_traffic.json (" + data["source"] + ")"
     except Exception as e:  # noqa: BLE001
         return None, f"no ncu capture ({type(e).__name__})"
 
