@@ -1,7 +1,7 @@
 #!/bin/bash
 # Evidence capture: plain bench (cfg2), ncu launch list of our kernels, ncu --set full of the
 # dominant kernels (one launch each).  Outputs in gpurun_out/ (summarised into profiles/).
-mkdir -p gpurun_out; rm -f gpurun_out/status.txt
+mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err; echo "bench=$?" >> gpurun_out/status.txt
 timeout 900 python bench.py --exact --no-cpu-baseline --no-scalar > gpurun_out/bench_cfg2_exact.json 2> gpurun_out/bench_cfg2_exact.err; echo "bench_exact=$?" >> gpurun_out/status.txt
 CMD="python bench.py --steps 5 --warmup 2 --no-cpu-baseline"
