@@ -256,21 +256,24 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     const uint32_t cell_off = need ? offsets[lin] : 0u;  // issued early: overlaps the atomic
     // lanes not emitting get a key no cell has, so MATCH runs on the full warp
     const unsigned peers = __match_any_sync(0xffffffffu, need ? lin : (0x80000000u | lane));
-    unsigned total = 0, prefix = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {  // k <= kMaxRun < 16
-      const unsigned mb = __ballot_sync(0xffffffffu, need && ((k >> b) & 1u)) & peers;
-      total += (unsigned)__popc(mb) << b;
-      prefix += (unsigned)__popc(mb & lt) << b;
-    }
     // Groups whose runs cover the same frames (the common case: image
     // neighbours crossing a cell together) take their slots frame-major --
     // (frame, pixel) = insertion order -- so the seal's sort finds them presorted.
     const unsigned leader = __ffs(peers) - 1;
     const uint32_t fk = (run_j << 4) | k;
     const uint32_t leader_fk = __shfl_sync(0xffffffffu, fk, leader);  // all lanes (full mask)
-    const bool differs = need && leader_fk != fk;
-    const bool uniform = (__ballot_sync(0xffffffffu, differs) & peers) == 0u;
+    const unsigned diff = __ballot_sync(0xffffffffu, need && leader_fk != fk);
+    const bool uniform = (diff & peers) == 0u;
+    unsigned total = __popc(peers) * k, prefix = 0;
+    if (diff != 0u) {  // some group mixes run shapes: slots by a bit-sliced prefix of the lengths
+      total = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {  // k <= kMaxRun < 16
+        const unsigned mb = __ballot_sync(0xffffffffu, need && ((k >> b) & 1u)) & peers;
+        total += (unsigned)__popc(mb) << b;
+        prefix += (unsigned)__popc(mb & lt) << b;
+      }
+    }
     unsigned base = 0;
     if (need && lane == leader) base = atomicAdd(&counts[lin], total);
     base = __shfl_sync(0xffffffffu, base, leader);
@@ -419,8 +422,7 @@ template <int kRun>
 struct SealSmem {
   uint32_t st[kRun * kPitch];  // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
   uint16_t sx[kRun * kPitch];  // its low key byte | z bin << 8, later | destination << 8
-  uint16_t cstart[32];         // cell start relative to the warp's first key
-  uint8_t cell_of[kRun * 32];  // key position -> lane of its cell
+  uint16_t pos_of[kRun * 32];  // key position -> (index in its cell) << 5 | lane of its cell
   float zb[3][32];             // z-quarter boundaries of each lane's cell (SampleRecords)
 };
 
@@ -472,8 +474,7 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
   const uint32_t len = s1 - s0;
   const bool staged = !__any_sync(0xffffffffu, big);  // then len <= 32 * 32
   if (staged) {
-    sm.cstart[lane] = (uint16_t)(cs - s0);
-    for (uint32_t k = 0; k < cn; ++k) sm.cell_of[cs - s0 + k] = (uint8_t)lane;
+    for (uint32_t k = 0; k < cn; ++k) sm.pos_of[cs - s0 + k] = (uint16_t)((k << 5) | lane);
     if constexpr (!Rec::kKeyBins) {
       const int64_t iz = (int64_t)c % bo.nz;
 #pragma unroll
@@ -494,8 +495,8 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
       for (int q = 0; q < 4; ++q) {
         const uint32_t i = i0 + 32u * q + lane;
         if (i < len) {
-          const uint32_t col = sm.cell_of[i];
-          const uint32_t at = (i - sm.cstart[col]) * kPitch + col;
+          const uint32_t pw = sm.pos_of[i], col = pw & 31u;
+          const uint32_t at = (pw >> 5) * kPitch + col;
           const uint32_t pid = (uint32_t)(kk[q] >> kKeyShift);
           uint32_t bin;
           if constexpr (Rec::kKeyBins) {
@@ -545,9 +546,9 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     }
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {
-      const uint32_t col = sm.cell_of[i];
-      const uint32_t j = i - sm.cstart[col], w = sm.sx[j * kPitch + col], dest = w >> 8;
-      records[s0 + sm.cstart[col] + dest] = rec(sm.st[j * kPitch + col], w & 0xffu);
+      const uint32_t pw = sm.pos_of[i], col = pw & 31u, j = pw >> 5;
+      const uint32_t w = sm.sx[j * kPitch + col], dest = w >> 8;
+      records[s0 + i - j + dest] = rec(sm.st[j * kPitch + col], w & 0xffu);
       bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
   } else if (cn > 0 && !big) {
