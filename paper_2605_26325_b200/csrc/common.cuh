@@ -179,9 +179,10 @@ __device__ __forceinline__ int64_t frame_cell(const double* fa, double U, double
   for (int a = 0; a < 3; ++a) {
     const double P = (U * fa[a] + V * fa[3 + a]) + fa[6 + a];
     const double d = (double)__double2float_rn(P) - m.origin[a];
-    const double f = floor(kInv ? d * m.inv_voxel : d / m.voxel);
-    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
-    idx[a] = ok ? (int)f : 0;
+    // 0 <= floor(q) < n  <=>  0 <= q < n (n integral; NaN fails both): no separate floor
+    const double q = kInv ? d * m.inv_voxel : d / m.voxel;
+    ok = ok && (q >= 0.0) && (q < (double)m.dims[a]);
+    idx[a] = ok ? (int)__double2uint_rz(q) : 0;
   }
   return ok ? ((int64_t)idx[0] * m.dims[1] + idx[1]) * m.dims[2] + idx[2] : -1;
 }

@@ -149,9 +149,10 @@ __device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, doub
     const float p32 = __double2float_rn((U * fa[a] + V * fa[3 + a]) + fa[6 + a]);
     if (a == 2) z32 = p32;
     const double d = (double)p32 - m.origin[a];
-    const double f = floor(kInv ? d * m.inv_voxel : d / m.voxel);
-    ok = ok && (f >= 0.0) && (f < (double)m.dims[a]);
-    idx[a] = ok ? (uint32_t)f : 0u;
+    // 0 <= floor(q) < n  <=>  0 <= q < n (n integral; NaN fails both): no separate floor
+    const double q = kInv ? d * m.inv_voxel : d / m.voxel;
+    ok = ok && (q >= 0.0) && (q < (double)m.dims[a]);
+    idx[a] = ok ? __double2uint_rz(q) : 0u;
   }
   iz = idx[2];
   return ok ? (int32_t)((idx[0] * (uint32_t)m.dims[1] + idx[1]) * (uint32_t)m.dims[2] + idx[2]) : -1;
