@@ -415,14 +415,19 @@ struct SampleRecords {
 
 constexpr int kSmallRun = 32;  // longest per-cell run sorted in shared memory by one lane
 constexpr int kSealWarps = 4;  // warps per seal block
-constexpr int kPitch = 33;     // odd row pitch: both access patterns conflict-free
+// Stage slot of the j-th key of the warp's cell `col`: rows of 32 with an XOR
+// swizzle.  Lane-per-cell loops (fixed j) touch a permutation of a row; the
+// key-per-lane passes (consecutive keys: runs of j within a cell, then the
+// next cell) hit distinct banks within a cell (2j mod 32 over <= 16 j) and
+// between neighbouring cells (col ^ 2j keeps col's parity).
+__device__ __forceinline__ uint32_t stage_at(uint32_t j, uint32_t col) { return j * 32u + (col ^ ((2u * j) & 31u)); }
 
 // kRun = the longest run the stage holds (16 or 32): the host picks 16 when no
 // cell has more samples (half the shared memory: 10 instead of 7 blocks/SM)
 template <int kRun>
 struct SealSmem {
-  uint32_t st[kRun * kPitch];  // st[k * kPitch + lane] = k-th insertion index of cell c0+lane
-  uint16_t sx[kRun * kPitch];  // its low key byte | z bin << 8, later | destination << 8
+  uint32_t st[kRun * 32];  // st[stage_at(k, lane)] = k-th insertion index of cell c0+lane
+  uint16_t sx[kRun * 32];  // its low key byte | z bin << 8, later | destination << 8
   uint16_t pos_of[kRun * 32];  // key position -> (index in its cell) << 5 | lane of its cell
   float zb[3][32];             // z-quarter boundaries of each lane's cell (SampleRecords)
 };
@@ -497,7 +502,7 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
         const uint32_t i = i0 + 32u * q + lane;
         if (i < len) {
           const uint32_t pw = sm.pos_of[i], col = pw & 31u;
-          const uint32_t at = (pw >> 5) * kPitch + col;
+          const uint32_t at = stage_at(pw >> 5, col);
           const uint32_t pid = (uint32_t)(kk[q] >> kKeyShift);
           uint32_t bin;
           if constexpr (Rec::kKeyBins) {
@@ -516,31 +521,31 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     // largest key so far: presorted runs (frame-major fill) cost one load each
     uint32_t top = cn ? sm.st[lane] : 0u;
     for (uint32_t i = 1; i < cn; ++i) {
-      const uint32_t x = sm.st[i * kPitch + lane];
+      const uint32_t x = sm.st[stage_at(i, lane)];
       if (x > top) {
         top = x;
         continue;
       }
-      const uint16_t xs = sm.sx[i * kPitch + lane];
+      const uint16_t xs = sm.sx[stage_at(i, lane)];
       uint32_t j = i;
       uint32_t y = top;  // st[j - 1] for j = i
       do {
-        sm.st[j * kPitch + lane] = y;
-        sm.sx[j * kPitch + lane] = sm.sx[(j - 1) * kPitch + lane];
+        sm.st[stage_at(j, lane)] = y;
+        sm.sx[stage_at(j, lane)] = sm.sx[stage_at(j - 1, lane)];
         --j;
-      } while (j > 0 && (y = sm.st[(j - 1) * kPitch + lane]) > x);
-      sm.st[j * kPitch + lane] = x;
-      sm.sx[j * kPitch + lane] = xs;
+      } while (j > 0 && (y = sm.st[stage_at(j - 1, lane)]) > x);
+      sm.st[stage_at(j, lane)] = x;
+      sm.sx[stage_at(j, lane)] = xs;
     }
     if (c < c_end) {  // lane = cell: stable destinations by bin, bins word
       // per-bin counters packed as bytes (runs <= 32): registers, not local memory
       uint32_t n = 0;
-      for (uint32_t j = 0; j < cn; ++j) n += 1u << (8u * (sm.sx[j * kPitch + lane] >> 8));
+      for (uint32_t j = 0; j < cn; ++j) n += 1u << (8u * (sm.sx[stage_at(j, lane)] >> 8));
       const uint32_t c1 = n & 0xffu, c2 = c1 + ((n >> 8) & 0xffu), c3 = c2 + ((n >> 16) & 0xffu);
       uint32_t next = (c1 << 8) | (c2 << 16) | (c3 << 24);  // byte b = first slot of bin b
       for (uint32_t j = 0; j < cn; ++j) {
-        const uint32_t w = sm.sx[j * kPitch + lane], sh = 8u * (w >> 8);
-        sm.sx[j * kPitch + lane] = (uint16_t)((w & 0xffu) | (((next >> sh) & 0xffu) << 8));
+        const uint32_t w = sm.sx[stage_at(j, lane)], sh = 8u * (w >> 8);
+        sm.sx[stage_at(j, lane)] = (uint16_t)((w & 0xffu) | (((next >> sh) & 0xffu) << 8));
         next += 1u << sh;
       }
       bo.bins[c] = c1 | (c2 << 8) | (c3 << 16) | (1u << 24);
@@ -548,8 +553,8 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t pw = sm.pos_of[i], col = pw & 31u, j = pw >> 5;
-      const uint32_t w = sm.sx[j * kPitch + col], dest = w >> 8;
-      records[s0 + i - j + dest] = rec(sm.st[j * kPitch + col], w & 0xffu);
+      const uint32_t w = sm.sx[stage_at(j, col)], dest = w >> 8;
+      records[s0 + i - j + dest] = rec(sm.st[stage_at(j, col)], w & 0xffu);
       bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
   } else if (cn > 0 && !big) {
