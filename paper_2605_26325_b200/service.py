@@ -164,14 +164,15 @@ class ResliceBatcher:
 
     `submit(msg)` validates on the caller's thread (errors become STATUS_ERROR
     responses, as process_request does) and returns a Future of the
-    ResliceResponse.  One dispatcher thread drains everything pending, groups
+    ResliceResponse.  A dispatcher thread drains everything pending, groups
     it by (width, height, config) in arrival order, and launches each group
-    (<= max_batch poses) once.  Results are the library's bit-for-bit: a
+    (<= max_batch poses) once; `workers` dispatchers overlap one batch's
+    launch with the collection of the next.  Results are the library's bit-for-bit: a
     pose's pixels do not depend on the other poses of its launch.
     """
 
     def __init__(self, volume, config: ResliceConfig | None = None, *, max_batch: int = 64,
-                 directional: bool | None = None):
+                 directional: bool | None = None, workers: int = 2):
         self.volume = volume
         self.config = config or ResliceConfig()
         self.max_batch = int(max_batch)
@@ -184,8 +185,15 @@ class ResliceBatcher:
         self._closed = False
         self.launches = 0
         self.requests = 0
-        self._thread = threading.Thread(target=self._loop, name="dare-batcher", daemon=True)
-        self._thread.start()
+        self._count_lock = threading.Lock()
+        # several dispatchers (each on its own CUDA stream): one drains and
+        # launches while the next batch is being collected by another
+        if int(workers) < 1:
+            raise InvalidArgumentError("workers must be >= 1")
+        self._threads = [threading.Thread(target=self._loop, name=f"dare-batcher-{i}", daemon=True)
+                         for i in range(int(workers))]
+        for t in self._threads:
+            t.start()
 
     # -- public ---------------------------------------------------------------
     def submit(self, msg) -> Future:
@@ -210,8 +218,9 @@ class ResliceBatcher:
     def close(self) -> None:
         with self._lock:
             self._closed = True
-            self._lock.notify()
-        self._thread.join()
+            self._lock.notify_all()
+        for t in self._threads:
+            t.join()
 
     def __enter__(self):
         return self
@@ -245,8 +254,9 @@ class ResliceBatcher:
 
                 pixels, cov = reslice_trilinear_batch(self.volume, planes)[:2]
                 bits = [pack_coverage(c) for c in cov]
-            self.launches += 1
-            self.requests += len(items)
+            with self._count_lock:
+                self.launches += 1
+                self.requests += len(items)
         except Exception as e:  # noqa: BLE001 -- every request gets an answer
             for p in items:
                 p.future.set_result(_error(p.msg, p.enqueued_at, str(e)))
