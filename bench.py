@@ -176,8 +176,8 @@ def ncu_traffic(kernel: str, batch: int, config: str):
         if config != "cfg2" or batch != 64:
             return None, "ncu capture is for cfg2 / 64 poses per launch"
         table = data["dram_bytes_per_launch"]
-        # ncu prints bool template arguments as 0/1
-        alt = kernel.replace("false", "0").replace("true", "1")
+        # (captures before the parts-per-pixel template argument printed it as the bool 0)
+        alt = kernel[:-2] + "0>" if kernel.endswith(", 1>") else kernel
         key = kernel if kernel in table else alt
         return float(table[key]), "profiles/round1_traffic.json (" + data["source"] + ")"
     except Exception as e:  # noqa: BLE001
@@ -613,7 +613,7 @@ def run_b200(args):
     else:
         n_or = int(info.n_orientations)
         gmode = 2 if n_or == 1 else (1 if schedule == 1 and n_or <= 1024 else 0)  # register / smem / global gate
-        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}, false>"
+        main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}, 1>"  # 1 part per pixel
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: prep_k (gate table + launch order; gate_k alone when not sorted), main
     # kernel, [fallback kernel on the certified path]

@@ -55,7 +55,7 @@ constexpr double kEx2Err = 4.76837158203125e-07;    // 2^-21
 constexpr double kSqrtErr = 4.76837158203125e-07;   // 2^-21
 constexpr double kMaxLog2Arg = 100.0;  // |weight exponent| (log2 units) the fast path accepts
 constexpr int kFastThreads = 128, kFastBlocks = 9;  // certified kernel: 36 warps/SM at 56 registers
-constexpr int kSplitMaxPoses = 4;      // pixel-major batches up to this size split pixels over 4 threads
+constexpr int kSplitMaxPoses = 4;      // pixel-major batches up to this size may split pixels (2 or 4 threads)
 constexpr size_t kArenaMax = 256ull << 20;  // larger scratch uses stream-ordered allocations
 
 struct ResliceArgs {
@@ -558,27 +558,35 @@ __device__ __forceinline__ bool certify(const ResliceArgs& a, double maxw, float
 
 // Certified path: same mapping as reslice_k; branch-free f32 weights for
 // every visited record (no warp rounds), 4 loads in flight, phased walk.
-// kSplit (small pixel-major batches, where one pose's 16x16-pixel blocks
-// cannot fill the GPU): 4 threads per pixel, each walking the column phases
-// p = part (mod 4); the order-independent certified sums are combined with
-// shuffles.  Block = 8x8 pixels, warp = 4x2 pixels x 4 parts.
-template <int kDistMode, int kGate, bool kSplit>
+// kParts > 1 (small pixel-major batches, where one pose's blocks cannot fill
+// the GPU): kParts threads per pixel, each walking the column phases
+// p = part (mod kParts); the order-independent certified sums are combined
+// with shuffles.  kParts 4: block 8x4 pixels, warp 4x2 pixels x 4 parts;
+// kParts 2: block 8x8 pixels, warp 4x4 pixels x 2 parts.
+template <int kDistMode, int kGate, int kParts>
 __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(ResliceArgs a,
                                                                            uint8_t* __restrict__ out,
                                                                            uint8_t* __restrict__ cov) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int pose, u, v;
   bool active;
-  const uint32_t part = kSplit ? (threadIdx.x & 3u) : 0u;
+  constexpr bool kSplit = kParts > 1;
+  const uint32_t part = kSplit ? (threadIdx.x & (uint32_t)(kParts - 1)) : 0u;
   {
     // 4 warps per block: pixel-major 16x8 pixels (warp 8x4), split 8x4 pixels
     // (warp 4x2 pixels x 4 parts), pose-major 4x1 pixels (warp = 32 poses)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (kSplit) {
+    if (kParts == 4) {
       const int pl = lane >> 2;
       pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
       u = (blockIdx.x % a.tiles_x) * 8 + (warp & 1) * 4 + (pl & 3);
       v = (blockIdx.x / a.tiles_x) * 4 + (warp >> 1) * 2 + (pl >> 2);
+      active = u < a.W && v < a.H;
+    } else if (kParts == 2) {
+      const int pl = lane >> 1;
+      pose = a.order ? a.order[blockIdx.y] : (int)blockIdx.y;
+      u = (blockIdx.x % a.tiles_x) * 8 + (warp & 1) * 4 + (pl & 3);
+      v = (blockIdx.x / a.tiles_x) * 8 + (warp >> 1) * 4 + (pl >> 2);
       active = u < a.W && v < a.H;
     } else if (a.pose_major) {
       pose = blockIdx.y * 32 + lane;
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
       active = u < a.W && v < a.H;
     }
   }
-  const uint32_t pmask = kSplit ? (0x111u << part) & 0x1ffu : 0x1ffu;
+  const uint32_t pmask = kParts == 4 ? (0x111u << part) & 0x1ffu : (kParts == 2 ? (0x155u << part) & 0x1ffu : 0x1ffu);
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
   const float g_single = kGate == kGateSingle ? __ldg(gate) : 0.0f;
   if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
@@ -675,9 +683,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
       i0 = w.s & ~1u;
     }
   }
-  if (kSplit) {  // the pixel's 4 partial sums (any order: the bound is order-free)
+  if (kSplit) {  // the pixel's partial sums (any order: the bound is order-free)
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
+    for (int o = 1; o < kParts; o <<= 1) {
       W += __shfl_xor_sync(0xffffffffu, W, o);
       J += __shfl_xor_sync(0xffffffffu, J, o);
       visits += __shfl_xor_sync(0xffffffffu, visits, o);
@@ -1085,14 +1093,18 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     set_smem(reslice_k<0>);
     set_smem(reslice_k<1>);
     set_smem(reslice_k<2>);
-    for (int sp = 0; sp < 2; ++sp) {
-      set_smem(sp ? reslice_fast_k<0, kGateGlobal, true> : reslice_fast_k<0, kGateGlobal, false>);
-      set_smem(sp ? reslice_fast_k<0, kGateSmem, true> : reslice_fast_k<0, kGateSmem, false>);
-      set_smem(sp ? reslice_fast_k<0, kGateSingle, true> : reslice_fast_k<0, kGateSingle, false>);
-      set_smem(sp ? reslice_fast_k<2, kGateGlobal, true> : reslice_fast_k<2, kGateGlobal, false>);
-      set_smem(sp ? reslice_fast_k<2, kGateSmem, true> : reslice_fast_k<2, kGateSmem, false>);
-      set_smem(sp ? reslice_fast_k<2, kGateSingle, true> : reslice_fast_k<2, kGateSingle, false>);
-    }
+    auto reg = [](auto parts) {
+      constexpr int S = decltype(parts)::value;
+      set_smem(reslice_fast_k<0, kGateGlobal, S>);
+      set_smem(reslice_fast_k<0, kGateSmem, S>);
+      set_smem(reslice_fast_k<0, kGateSingle, S>);
+      set_smem(reslice_fast_k<2, kGateGlobal, S>);
+      set_smem(reslice_fast_k<2, kGateSmem, S>);
+      set_smem(reslice_fast_k<2, kGateSingle, S>);
+    };
+    reg(std::integral_constant<int, 1>{});
+    reg(std::integral_constant<int, 2>{});
+    reg(std::integral_constant<int, 4>{});
   });
   if (!fast) {
     if (a.dist_mode == 0)
@@ -1108,12 +1120,34 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   DARE_CUDA(cudaMemsetAsync(a.amb_count, 0, sizeof(unsigned), s));
   const int gmode = a.n_orient == 1 ? kGateSingle
                                     : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal);
-  // small pixel-major batches: split pixels over 4 threads
-  const bool split = !a.pose_major && P <= kSplitMaxPoses;
+  // small pixel-major batches: split pixels over 2 or 4 threads.  Cost model:
+  // waves of resident warps x column phases per thread (9 / 5 / 3 for 1 / 2 /
+  // 4 parts).  Measured at cfg2 (256x256 poses, us per launch, 1 / 2 / 4
+  // parts): P=1 116 / 94 / 111, P=2 126 / 143 / 171, P=4 191 / 228 / 267 --
+  // the model's choice each time (tools/split_probe.py).
+  int parts = 1;
+  if (!a.pose_major && P <= kSplitMaxPoses) {
+    const uint64_t cap = (uint64_t)sm_count() * kFastBlocks * (kFastThreads / 32);
+    const uint64_t npix = (uint64_t)P * W * H;
+    uint64_t best = ~0ull;
+    for (int sp : {1, 2, 4}) {
+      const uint64_t warps = (npix * sp + 31) / 32;
+      const uint64_t cost = ((warps + cap - 1) / cap) * (sp == 4 ? 3 : (sp == 2 ? 5 : 9));
+      if (cost < best) {
+        best = cost;
+        parts = sp;
+      }
+    }
+    const char* e = getenv("DARE_SPLIT");  // development override (1, 2 or 4)
+    if (e) parts = atoi(e) == 2 ? 2 : (atoi(e) == 1 ? 1 : 4);
+  }
   dim3 kgrid;
-  if (split) {
+  if (parts == 4) {
     a.tiles_x = (int)ceil_div(W, 8);
     kgrid = dim3(a.tiles_x * ceil_div(H, 4), P);
+  } else if (parts == 2) {
+    a.tiles_x = (int)ceil_div(W, 8);
+    kgrid = dim3(a.tiles_x * ceil_div(H, 8), P);
   } else if (a.pose_major) {
     a.tiles_x = (int)ceil_div(W, 4);
     kgrid = dim3(a.tiles_x * H, ceil_div(P, 32));
@@ -1123,13 +1157,15 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   }
   auto pick = [&](auto dm) {
     constexpr int D = decltype(dm)::value;
-    if (split)
-      return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, true>
-                                  : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, true>
-                                                        : reslice_fast_k<D, kGateGlobal, true>);
-    return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, false>
-                                : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, false>
-                                                      : reslice_fast_k<D, kGateGlobal, false>);
+    auto by_gate = [&](auto sp) {
+      constexpr int S = decltype(sp)::value;
+      return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, S>
+                                  : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, S>
+                                                        : reslice_fast_k<D, kGateGlobal, S>);
+    };
+    return parts == 4 ? by_gate(std::integral_constant<int, 4>{})
+                      : (parts == 2 ? by_gate(std::integral_constant<int, 2>{})
+                                    : by_gate(std::integral_constant<int, 1>{}));
   };
   auto k = a.dist_mode == 2 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 0>{});
   k<<<kgrid, kFastThreads, kSmemBytes, s>>>(a, d_pixels, d_cov);

@@ -487,3 +487,23 @@ def test_fallback_wide_neighbourhoods(rng, radius):
     one = _reslice_raw(vol, planes[:1], cfg, False)
     np.testing.assert_array_equal(one[0][0], ex[0][0])
     np.testing.assert_array_equal(one[1][0], ex[1][0])
+
+
+@pytest.mark.parametrize("parts", ["1", "2", "4"])
+def test_split_pixel_variants_identical(rng, parts, monkeypatch):
+    """Small batches split a pixel's column phases over 1, 2 or 4 threads (host
+    cost model; DARE_SPLIT forces one): same bits as the oracle for each."""
+    vol = _random_volume(rng, 30000, 10.0, 0.25)
+    cfg = ResliceConfig(interp_radius=0.25, normal_threshold_deg=70, inplane_threshold_deg=70)
+    planes = []
+    for _ in range(3):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        planes.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(2, 8, 3)), 37, 29, (0.2, 0.2)))
+    monkeypatch.setenv("DARE_SPLIT", parts)
+    for P in (1, 3):
+        px, cov, _ = db.reslice_batch(vol, planes[:P], cfg)
+        for k in range(P):
+            ref = oracle.reslice(vol, oracle.plane_params(planes[k]), oracle.cfg_array(cfg), 37, 29)
+            np.testing.assert_array_equal(px[k], ref[0])
+            np.testing.assert_array_equal(cov[k], ref[1])
