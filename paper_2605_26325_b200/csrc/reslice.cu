@@ -745,6 +745,9 @@ __device__ __forceinline__ bool exact_sums_flat(const Walk& w, const ResliceArgs
     if (lane >= o) incl += t;
   }
   const uint32_t V = __shfl_sync(0xffffffffu, incl, (int)ncol - 1);
+  // pass 1: loads, cube and gate tests, in-order compaction of the survivor
+  // RECORDS into shared memory (the sw / swi space of this warp, 16 B each)
+  uint4* srec = reinterpret_cast<uint4*>(sw);  // kFlatCap records = the sw + swi bytes (contiguous)
   uint32_t cnt = 0;
   constexpr int kU = 4;  // chunks of 32 positions in flight per iteration
   for (uint32_t q0 = 0; q0 < V; q0 += 32 * kU) {  // warp-uniform trip count
@@ -769,25 +772,49 @@ __device__ __forceinline__ bool exact_sums_flat(const Walk& w, const ResliceArgs
       c[t] = in[t] ? __ldg(a.records + canon_to_store(a.perm, col_start + (q - col_excl)))
                    : make_uint4(0, 0, 0, 0);
     }
-    bool keep[kU];
-    double wt[kU];
 #pragma unroll
-    for (int t = 0; t < kU; ++t) {  // then the (independent) FP64 weights
-      keep[t] = in[t] && w.in_cube(c[t]) && gate[c[t].w >> 8] != CUDART_INF;
-      wt[t] = keep[t] ? exact_weight<kDistMode>(a, w, c[t], gate) : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < kU; ++t) {  // and the in-order compaction
-      const unsigned m = __ballot_sync(0xffffffffu, keep[t]);
+    for (int t = 0; t < kU; ++t) {  // in-order compaction of the survivors
+      const bool keep = in[t] && w.in_cube(c[t]) && gate[c[t].w >> 8] != CUDART_INF;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
       const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1u));
-      if (keep[t] && pos < (uint32_t)kFlatCap) {
-        sw[pos] = wt[t];
-        swi[pos] = wt[t] * (double)(c[t].w & 0xffu);
-      }
+      if (keep && pos < (uint32_t)kFlatCap) srec[pos] = c[t];
       cnt += __popc(m);
     }
   }
   if (cnt > (uint32_t)kFlatCap) return false;
+  __syncwarp();
+  // pass 2: the FP64 weights of the survivors only (lane j: survivors j, j+32, ...),
+  // kept in registers until every record has been read, then written in order
+  constexpr int kR = kFlatCap / 32;
+  double wt[kR], wi[kR];
+  const uint32_t rounds = (cnt + 31) / 32;
+#pragma unroll
+  for (int g = 0; g < kR; g += 4) {  // four independent FP64 chains per step (latency)
+    if ((uint32_t)g < rounds) {
+      uint4 c[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) c[t] = srec[min((uint32_t)(32 * (g + t) + lane), cnt - 1)];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool ok = (uint32_t)(32 * (g + t) + lane) < cnt;
+        const double x = exact_weight<kDistMode>(a, w, c[t], gate);
+        wt[g + t] = ok ? x : 0.0;
+        wi[g + t] = ok ? x * (double)(c[t].w & 0xffu) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) wt[g + t] = wi[g + t] = 0.0;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const uint32_t j = (uint32_t)(32 * r + lane);
+    if (j < cnt) {
+      sw[j] = wt[r];
+      swi[j] = wi[r];
+    }
+  }
   __syncwarp();
   double ws = 0.0, is = 0.0;
   if (lane == 0)
@@ -806,7 +833,9 @@ __device__ __forceinline__ bool exact_sums_flat(const Walk& w, const ResliceArgs
 template <int kDistMode>
 __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t* __restrict__ out,
                                                        uint8_t* __restrict__ cov) {
-  __shared__ double s_w[8][kFlatCap], s_wi[8][kFlatCap];
+  // per warp: kFlatCap weights then kFlatCap weighted intensities, contiguous
+  // (exact_sums_flat first stages up to kFlatCap 16 B survivor records there)
+  __shared__ __align__(16) double s_buf[8][2 * kFlatCap];
   const unsigned n = *a.amb_count;
   const bool all = n > a.amb_cap;
   const uint64_t total = all ? (uint64_t)a.P * a.H * a.W : (uint64_t)n;
@@ -824,7 +853,7 @@ __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t
     double wsum, iwsum;
     const double* gate = a.gate + (size_t)pose * a.n_orient;
     const int wid = threadIdx.x >> 5;
-    if (!exact_sums_flat<kDistMode>(w, a, gate, s_w[wid], s_wi[wid], wsum, iwsum))
+    if (!exact_sums_flat<kDistMode>(w, a, gate, s_buf[wid], s_buf[wid] + kFlatCap, wsum, iwsum))
       exact_sums_warp<kDistMode>(w, a, gate, wsum, iwsum);  // > 32 columns / many survivors
     if ((threadIdx.x & 31) == 0) write_exact(a, k, wsum, iwsum, out, cov);
   }
