@@ -187,14 +187,15 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   int32_t cur = -1;
-  uint32_t run_j = 0, k = 0, bb = 0, nr = 0;
+  uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_oob = 0;
   float zb1 = 0.f, zb2 = 0.f, zb3 = 0.f;  // z-quarter bounds of the run's cell
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count
     float z = 0.f;
     uint32_t iz = 0;
-    const int32_t lin = in_frame ? frame_cell32<kInv>(s_axes + j * 9, U, V, m, z, iz) : -1;
-    const unsigned oob = __ballot_sync(0xffffffffu, in_frame && lin < 0);
-    if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)__popc(oob));
+    // computed for every lane (no divergent branch), then masked
+    const int32_t cell = frame_cell32<kInv>(s_axes + j * 9, U, V, m, z, iz);
+    const int32_t lin = in_frame ? cell : -1;
+    n_oob += (in_frame && cell < 0) ? 1u : 0u;
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     if (restart && cur >= 0) {
       atomicAdd(&counts[cur], k);
@@ -221,6 +222,8 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
     ++nr;
   }
   nruns[blk * 256 + threadIdx.x] = (uint8_t)nr;  // <= kRunFrames
+  const unsigned oob = __reduce_add_sync(0xffffffffu, n_oob);  // one atomic per warp
+  if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
 }
 
 // Fill pass over the chunks [chunk_begin, chunk_begin + gridDim.y): replays
