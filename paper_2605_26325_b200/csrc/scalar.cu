@@ -81,12 +81,10 @@ __global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m
   int64_t cur = -1;
   unsigned sum = 0, cnt = 0;
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count
-    int64_t lin = -1;
-    unsigned inten = 0;
-    if (in_frame) {
-      lin = frame_cell<kInv>(s_axes + j * 9, U, V, m);
-      inten = fv.frames[s_img[j] + p];
-    }
+    // the cell is computed for every lane (no divergent branch) and masked
+    const int64_t cell = frame_cell<kInv>(s_axes + j * 9, U, V, m);
+    const int64_t lin = in_frame ? cell : -1;
+    const unsigned inten = in_frame ? (unsigned)fv.frames[s_img[j] + p] : 0u;
     const bool change = lin != cur;
     const bool need = change && cur >= 0;
     if (__any_sync(0xffffffffu, need)) compound_flush(need, cur, sum, cnt, sums, counts);
