@@ -85,13 +85,19 @@ struct ResliceArgs {
   unsigned* amb_count;
   unsigned amb_cap;
   unsigned long long* fallback_total;  // optional running count (stats)
+  // small unsorted pixel-major launches: each block computes its pose's gate
+  // row itself (no gate_k launch on the latency path); blocks x == 0 also
+  // store it to gate / gate2 for the fallback kernel
+  int inline_gate;
+  const float4* orient;
+  dare_reslice_cfg cfg;
 };
 
 // gate table: one thread per (orientation, pose); the certified path's f32
 // copy is pre-scaled to log2 units.
-__device__ __forceinline__ void gate_one(const float4* __restrict__ orient, int64_t n_orient,
-                                         const double* __restrict__ params, int64_t o, int p,
-                                         const dare_reslice_cfg& cfg, double* gate, float* gate2) {
+__device__ __forceinline__ double gate_value(const float4* __restrict__ orient,
+                                            const double* __restrict__ params, int64_t o, int p,
+                                            const dare_reslice_cfg& cfg) {
   const double* pp = params + (size_t)p * 14;
   const double xrx = pp[3], xry = pp[6], xrz = pp[9];   // R[:,0]
   const double nrx = pp[5], nry = pp[8], nrz = pp[11];  // R[:,2]
@@ -109,6 +115,13 @@ __device__ __forceinline__ void gate_one(const float4* __restrict__ orient, int6
     double di = fabs((xsx * xrx + xsy * xry) + xsz * xrz);
     if (!(di < cfg.cos_inplane)) A = cfg.k_normal * (dn - 1.0) + cfg.k_inplane * (di - 1.0);
   }
+  return A;
+}
+
+__device__ __forceinline__ void gate_one(const float4* __restrict__ orient, int64_t n_orient,
+                                         const double* __restrict__ params, int64_t o, int p,
+                                         const dare_reslice_cfg& cfg, double* gate, float* gate2) {
+  const double A = gate_value(orient, params, o, p, cfg);
   gate[(size_t)p * n_orient + o] = A;
   gate2[(size_t)p * n_orient + o] = __double2float_rn(A * kLog2e);
 }
@@ -603,12 +616,28 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   }
   const uint32_t pmask = kParts == 4 ? (0x111u << part) & 0x1ffu : (kParts == 2 ? (0x155u << part) & 0x1ffu : 0x1ffu);
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
-  const float g_single = kGate == kGateSingle ? __ldg(gate) : 0.0f;
-  if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
+  float g_single = 0.0f;
+  if (kGate != kGateGlobal && kParts > 1 && a.inline_gate) {  // one pose per block: the row computed here
     float* sg = reinterpret_cast<float*>(smem_raw);
-    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) sg[i] = gate[i];
+    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
+      const double A = gate_value(a.orient, a.params, i, pose, a.cfg);
+      sg[i] = __double2float_rn(A * kLog2e);
+      if (blockIdx.x == 0) {
+        const_cast<double*>(a.gate)[(size_t)pose * a.n_orient + i] = A;
+        const_cast<float*>(a.gate2)[(size_t)pose * a.n_orient + i] = sg[i];
+      }
+    }
     __syncthreads();
     gate = sg;
+    if (kGate == kGateSingle) g_single = sg[0];
+  } else {
+    if (kGate == kGateSingle) g_single = __ldg(gate);
+    if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
+      float* sg = reinterpret_cast<float*>(smem_raw);
+      for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) sg[i] = gate[i];
+      __syncthreads();
+      gate = sg;
+    }
   }
   FastWalk w;
   float wh[3], wl[3];
@@ -1093,6 +1122,12 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.amb = cv.take<unsigned long long>(a.amb_cap);
   a.amb_count = cv.take<unsigned>(1);
   a.order = nullptr;
+  a.orient = vol->d_orient;
+  a.cfg = *cfg;
+  // latency path (small unsorted pixel-major certified launches, single or
+  // shared-memory gate): the gate row is computed inside reslice_fast_k
+  a.inline_gate = fast && !sorted && !a.pose_major && vol->n_orient > 0 && vol->n_orient <= kGateSmemF ? 1 : 0;
+  // (set per launch below: only the split kernels compute the row inline)
   const bool rank_sort = sorted && P <= kRankSortMax;
   if (rank_sort) {  // gate table and launch order in one launch
     prep_k<<<dim3(std::max<unsigned>(1u, ceil_div(vol->n_orient, 256)), P + 1), 256,
@@ -1101,7 +1136,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
                                                   a.origin[1], a.origin[2], 8.0 * a.voxel, order);
     DARE_CUDA(cudaGetLastError());
     a.order = order;
-  } else if (vol->n_orient > 0) {
+  } else if (vol->n_orient > 0 && !a.inline_gate) {
     gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient,
                                                                  d_params, P, *cfg, (double*)a.gate,
                                                                  (float*)a.gate2);
@@ -1169,6 +1204,12 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     }
     const char* e = getenv("DARE_SPLIT");  // development override (1, 2 or 4)
     if (e) parts = atoi(e) == 2 ? 2 : (atoi(e) == 1 ? 1 : 4);
+  }
+  if (parts == 1 && a.inline_gate) {  // the unsplit kernel reads the table: compute it first
+    a.inline_gate = 0;
+    gate_k<<<dim3(ceil_div(vol->n_orient, 256), P), 256, 0, s>>>(vol->d_orient, vol->n_orient, d_params, P,
+                                                                 *cfg, (double*)a.gate, (float*)a.gate2);
+    DARE_CUDA(cudaGetLastError());
   }
   dim3 kgrid;
   if (parts == 4) {
