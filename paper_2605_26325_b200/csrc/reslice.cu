@@ -1318,13 +1318,15 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   const size_t npix = (size_t)n_poses * width * height;
   // call buffers from the thread's arena (slot 1; launch scratch uses slot 0)
   const size_t hw = (size_t)width * height, bpp = (hw + 7) / 8, nbits = (size_t)n_poses * bpp;
-  const size_t total = Carve::up(sizeof(double) * 14 * n_poses) + Carve::up(2 * npix) +
-                       Carve::up(sizeof(unsigned long long)) + (packed ? Carve::up(nbits) : 0);
+  // device outputs laid out [pixels | coverage | pad | fallback count]: one D2H copy when staged
+  const size_t fbo = (2 * npix + 7) & ~(size_t)7;
+  const size_t total = Carve::up(sizeof(double) * 14 * n_poses) + Carve::up(fbo + sizeof(unsigned long long)) +
+                       (packed ? Carve::up(nbits) : 0);
   Scratch<uint8_t> block(total > kArenaMax ? total : 0, s);
   Carve cv{total > kArenaMax ? block.ptr : (uint8_t*)thread_arena(1, total, s)};
   double* d_params = cv.take<double>((size_t)n_poses * 14);
-  uint8_t* d_out = cv.take<uint8_t>(2 * npix);
-  unsigned long long* d_fb = cv.take<unsigned long long>(1);
+  uint8_t* d_out = cv.take<uint8_t>(fbo + sizeof(unsigned long long));
+  unsigned long long* d_fb = reinterpret_cast<unsigned long long*>(d_out + fbo);
   uint8_t* d_bits = packed ? cv.take<uint8_t>(nbits) : nullptr;
   DARE_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), s));
   // small calls from pageable memory (the latency path): stage through the
@@ -1332,7 +1334,7 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   const size_t out_bytes = npix + (packed ? nbits : npix);
   const bool stage = out_bytes <= kStageMax && !host_pinned(pixels);
   const size_t pbytes = sizeof(double) * 14 * n_poses;
-  uint8_t* h_stage = stage ? (uint8_t*)thread_pinned(pbytes + out_bytes + sizeof(unsigned long long)) : nullptr;
+  uint8_t* h_stage = stage ? (uint8_t*)thread_pinned(pbytes + fbo + sizeof(unsigned long long) + nbits) : nullptr;
   const double* h_params = params;
   if (stage) {
     memcpy(h_stage, params, pbytes);
@@ -1349,18 +1351,21 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   unsigned long long fb = 0;
   const size_t cov_bytes = packed ? nbits : npix;
   uint8_t* h_px = stage ? h_stage + pbytes : pixels;
-  uint8_t* h_cov = stage ? h_px + npix : coverage;
-  unsigned long long* h_fb = stage ? (unsigned long long*)(h_cov + cov_bytes) : &fb;
-  DARE_CUDA(cudaMemcpyAsync(h_px, d_out, npix, cudaMemcpyDeviceToHost, s));
+  uint8_t* h_cov = stage ? (packed ? h_px + fbo + sizeof(unsigned long long) : h_px + npix) : coverage;
+  unsigned long long* h_fb = stage ? reinterpret_cast<unsigned long long*>(h_px + fbo) : &fb;
+  if (stage && !packed) {  // pixels, coverage and the fallback count in one copy
+    DARE_CUDA(cudaMemcpyAsync(h_px, d_out, fbo + sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  } else {
+    DARE_CUDA(cudaMemcpyAsync(h_px, d_out, npix, cudaMemcpyDeviceToHost, s));
+    if (!packed) DARE_CUDA(cudaMemcpyAsync(h_cov, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaMemcpyAsync(h_fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
+  }
   if (packed) {
     pack_coverage_k<<<ceil_div(nbits, 256), 256, 0, s>>>(d_out + npix, (int64_t)hw, (int64_t)bpp,
                                                         (int64_t)nbits, d_bits);
     DARE_CUDA(cudaGetLastError());
     DARE_CUDA(cudaMemcpyAsync(h_cov, d_bits, nbits, cudaMemcpyDeviceToHost, s));
-  } else {
-    DARE_CUDA(cudaMemcpyAsync(h_cov, d_out + npix, npix, cudaMemcpyDeviceToHost, s));
   }
-  DARE_CUDA(cudaMemcpyAsync(h_fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
   DARE_CUDA(cudaStreamSynchronize(s));
   if (stage) {
     memcpy(pixels, h_px, npix);
