@@ -101,10 +101,12 @@ void* thread_pinned(size_t bytes) {
   };
   static thread_local Pinned b;
   if (b.cap < bytes) {
+    const size_t old_cap = b.cap;
     if (b.p) DARE_CUDA(cudaFreeHost(b.p));
     b.p = nullptr;
     b.cap = 0;
-    const size_t want = std::max<size_t>(bytes, 1 << 20);
+    // geometric growth: pinned allocations are slow and cudaFreeHost synchronises
+    const size_t want = std::max<size_t>(std::max<size_t>(bytes, 8u << 20), 2 * old_cap);
     DARE_CUDA(cudaMallocHost(&b.p, want));
     b.cap = want;
   }
