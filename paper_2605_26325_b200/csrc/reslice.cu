@@ -865,6 +865,9 @@ __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t
   // per warp: kFlatCap weights then kFlatCap weighted intensities, contiguous
   // (exact_sums_flat first stages up to kFlatCap 16 B survivor records there)
   __shared__ __align__(16) double s_buf[8][2 * kFlatCap];
+  // launched as a programmatic dependent of reslice_fast_k: the blocks are
+  // resident before it finishes, and wait here for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const unsigned n = *a.amb_count;
   const bool all = n > a.amb_cap;
   const uint64_t total = all ? (uint64_t)a.P * a.H * a.W : (uint64_t)n;
@@ -1242,12 +1245,24 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   pt.mark("reslice_fast_k");
   DARE_CUDA(cudaGetLastError());
   const unsigned fb_grid = (unsigned)sm_count() * 2;
-  if (a.dist_mode == 0)
-    reslice_fallback_k<0><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
-  else if (a.dist_mode == 1)
-    reslice_fallback_k<1><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
-  else
-    reslice_fallback_k<2><<<fb_grid, 256, 0, s>>>(a, d_pixels, d_cov);
+  {  // programmatic dependent launch: overlaps the fallback's launch with the main kernel's tail
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(fb_grid);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (a.dist_mode == 0)
+      DARE_CUDA(cudaLaunchKernelEx(&lc, reslice_fallback_k<0>, a, d_pixels, d_cov));
+    else if (a.dist_mode == 1)
+      DARE_CUDA(cudaLaunchKernelEx(&lc, reslice_fallback_k<1>, a, d_pixels, d_cov));
+    else
+      DARE_CUDA(cudaLaunchKernelEx(&lc, reslice_fallback_k<2>, a, d_pixels, d_cov));
+  }
   pt.mark("fallback");
   DARE_CUDA(cudaGetLastError());
 }
