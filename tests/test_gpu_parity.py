@@ -69,6 +69,25 @@ def test_reconstruct_random_sweeps_match_oracle(seed, voxel, margin):
     assert_volume_equal(v, oracle.reconstruct(rec, voxel, margin))
 
 
+def test_reconstruct_host_frames_many_upload_groups():
+    """A linear sweep long enough for several 64-frame chunks: host frames upload in groups and
+    the fill runs one launch per group; frames on the device take one fill launch.  Both equal
+    the oracle (insertion order across chunk and group boundaries)."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    n, h, w = 300, 12, 14
+    poses = [Pose(Quaternion.from_axis_angle((1, 0.2, 0), 0.002 * k), (0.0, 0.0, 0.021 * k)) for k in range(n)]
+    ts = np.arange(n) * 0.03
+    rec = db.SweepRecording(rng.integers(0, 256, (n, h, w), dtype=np.uint8), ts, ts, poses, (0.1, 0.1))
+    ref = oracle.reconstruct(rec, 0.2, 0.3)
+    assert_volume_equal(db.reconstruct_volume(rec, voxel_size=0.2, margin=0.3), ref)
+    frames_d = torch.from_numpy(np.asarray(rec.images)).cuda()
+    dev = db.SweepRecording(np.asarray(rec.images), ts, ts, poses, (0.1, 0.1))
+    v = db.reconstruct_volume(dev, voxel_size=0.2, margin=0.3, frames_device_ptr=frames_d.data_ptr())
+    assert_volume_equal(v, ref)
+
+
 def test_reconstruct_dense_cells_use_large_run_path():
     # many frames at one pose: > 32 samples per cell -> segmented-sort path
     rng = np.random.default_rng(5)
