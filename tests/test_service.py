@@ -163,3 +163,17 @@ def test_batcher_serves_trilinear(rng):
         assert res.status == svc.STATUS_OK
         assert res.image == one.pixels.tobytes()
         assert res.coverage == np.packbits(one.coverage, axis=None).tobytes()
+
+
+@pytest.mark.gpu
+def test_reslice_packed_large_batch_unstaged(rng):
+    """> 4 MB of output: the unstaged host-buffer path (direct copies) of dare_reslice_packed."""
+    vol = _volume(rng, n=20000)
+    cfg = ResliceConfig(interp_radius=0.5, normal_threshold_deg=80, inplane_threshold_deg=80)
+    planes = [ReslicePlane(Pose(Quaternion(*_pose7(rng)[3:]), rng.uniform(1, 7, 3)), 256, 256, (0.03, 0.03))
+              for _ in range(70)]
+    px, bits, _ = svc.reslice_packed(vol, planes, cfg)
+    ref_px, ref_cov, _ = db.reslice_batch(vol, planes, cfg)
+    np.testing.assert_array_equal(px, ref_px)
+    for k in range(len(planes)):
+        assert bits[k].tobytes() == np.packbits(ref_cov[k], axis=None).tobytes()
