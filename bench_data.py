@@ -10,11 +10,11 @@ rotation about x by U(-10, 10) deg, translation (0, 0, L*(0.1 + 0.8 U));
 cfg4 is a 10k-pose haptic-style trajectory on the cfg3 volume (random-walk
 centre with N(0, 0.05 mm) steps reflected inside the cube, base orientation
 cycling A -> B -> C -> D every 2500 poses plus a bounded +-20 deg tilt random
-walk with 0.2 deg steps).  Image content is a synthetic phantom (background 24,
-spherical inclusions, speckle) rendered on the GPU with torch -- the reference's
-CPU renderer takes ~2 min for cfg2 and ~16 min for cfg3; content does not
-change the work the hot path does (every pixel is scattered, every visited
-sample is evaluated).
+walk with 0.2 deg steps).  Image content is the reference's benchmark phantom
+(phantom.py:402-467 default_benchmark_scene: vessels, sphere, two-sided slab,
+speckle seed 7 amplitude 5), render_intensities (phantom.py:113-152) restated
+in torch f64 on the GPU with numpy's own per-frame speckle streams -- the
+reference's CPU renderer takes ~2 min for cfg2 and ~16 min for cfg3.
 """
 from __future__ import annotations
 
@@ -88,44 +88,137 @@ def sweep_poses(wl: Workload):
     return poses, np.concatenate(ts)
 
 
-def render_frames_torch(wl: Workload, device="cuda", seed=7):
-    """(n, H, W) u8 frames on the device: background 24, three spheres, speckle,
-    sampled at each frame's world pixel positions."""
+# ---------------------------------------------------------------- phantom content
+# The reference's benchmark scene (phantom.py:402-467 default_benchmark_scene,
+# seed 7, speckle 5): background 24, specular exponent 4, two vessel tubes, a
+# sphere and a tilted two-sided reflector slab (scene_from_dict, phantom.py:308-348).
+_W96, _P96 = 96, 0.25
+_CX = 0.5 * (_W96 - 1) * _P96
+_DEPTH = (_W96 - 1) * _P96
+_SWEEP_LEN = 28.0
+SCENE = dict(
+    background=24.0, specular=4.0, speckle=5.0, seed=7,
+    inclusions=[
+        ("tube", dict(point=(_CX, 0.45 * _DEPTH, 0.0), direction=(0.0, 0.0, 1.0), radius=4.2, intensity=195.0,
+                      back=None, wall=0.9)),
+        ("tube", dict(point=(_CX - 6.5, 0.72 * _DEPTH, 0.0), direction=(0.2, 0.0, 1.0), radius=2.4,
+                      intensity=165.0, back=None, wall=0.8)),
+        ("sphere", dict(center=(_CX + 6.0, 0.3 * _DEPTH, 0.45 * _SWEEP_LEN), radius=3.4, intensity=225.0,
+                        back=None, wall=0.9)),
+        ("slab", dict(point=(_CX, 0.9 * _DEPTH, 0.0), normal=(0.0, -1.0, 0.15), intensity=90.0, back=190.0,
+                      wall=0.8)),
+    ],
+)
+
+
+def frame_keys(wl: Workload) -> np.ndarray:
+    """phantom.simulate_sweep seeds speckle with frame_key = index within its
+    sweep (phantom.py:226-231); merge_recordings concatenates sweeps."""
+    per = wl.n_frames // wl.sweeps
+    return np.concatenate([np.arange(per) for _ in range(wl.sweeps)])
+
+
+def speckle(key: int, shape, scene=SCENE) -> np.ndarray:
+    """The reference's per-frame speckle stream (phantom.py:149-151)."""
+    rng = np.random.default_rng((scene["seed"], int(key)))
+    return rng.normal(0.0, scene["speckle"], shape)
+
+
+def _norm3(x, y, z, torch):
+    return torch.sqrt((x * x + y * y) + z * z)
+
+
+def render_phantom(poses, width: int, height: int, pitch, keys, device="cuda", scene=SCENE, noise=True,
+                   threads: int = 0):
+    """(n, H, W) u8 frames: phantom.render_intensities (phantom.py:113-152) for
+    `poses` restated with torch in f64 on `device` (same expressions and
+    evaluation order; the speckle is numpy's own per-frame generator, drawn on
+    host threads).  Equal to the reference's frames except where an f64
+    rounding difference (pow / dot order) moves a value across a rint tie
+    (tests/test_bench_phantom.py measures it)."""
+    import concurrent.futures
+    import os
+
     import torch
 
     from paper_2605_26325_b200.geometry import rotation_matrix
 
+    n = len(poses)
+    px, py = pitch
+    f64 = dict(dtype=torch.float64, device=device)
+    u = torch.arange(width, **f64) * px
+    v = torch.arange(height, **f64) * py
+    out = torch.empty((n, height, width), dtype=torch.uint8, device=device)
+    prims = []
+    for kind, a in scene["inclusions"]:
+        if kind == "tube":
+            d = np.asarray(a["direction"], dtype=float)
+            d = d / np.linalg.norm(d)
+            prims.append((kind, np.asarray(a["point"], float), d, a))
+        elif kind == "sphere":
+            prims.append((kind, np.asarray(a["center"], float), None, a))
+        else:
+            nn = np.asarray(a["normal"], dtype=float)
+            nn = nn / np.linalg.norm(nn)
+            prims.append((kind, np.asarray(a["point"], float), nn, a))
+    pool = concurrent.futures.ThreadPoolExecutor(threads or min(32, os.cpu_count() or 1)) if noise else None
+    chunk = 32
+    try:
+        pending = None
+        if noise:
+            pending = [pool.submit(speckle, int(keys[i]), (height, width), scene) for i in range(min(chunk, n))]
+        for k0 in range(0, n, chunk):
+            k1 = min(n, k0 + chunk)
+            nxt = None
+            if noise and k1 < n:
+                nxt = [pool.submit(speckle, int(keys[i]), (height, width), scene)
+                       for i in range(k1, min(n, k1 + chunk))]
+            R = torch.tensor(np.array([rotation_matrix(p.rotation) for p in poses[k0:k1]]), **f64)
+            T = torch.tensor(np.array([p.translation for p in poses[k0:k1]], dtype=float), **f64)
+            xa, ya = R[:, :, 0], R[:, :, 1]  # frame_axes: x = R[:,0], y = R[:,1] (= beam)
+            # pts = (u * x_axis + v * y_axis) + t, per component
+            P = [(u[None, None, :] * xa[:, c, None, None] + v[None, :, None] * ya[:, c, None, None])
+                 + T[:, c, None, None] for c in range(3)]
+            img = torch.full((k1 - k0, height, width), float(scene["background"]), **f64)
+            for kind, anchor, d, a in prims:
+                rel = [P[c] - float(anchor[c]) for c in range(3)]
+                if kind == "sphere":
+                    dist = _norm3(*rel, torch)
+                    safe = torch.clamp(dist, min=1e-9)
+                    nrm = [rel[c] / safe for c in range(3)]
+                    shell = torch.abs(dist - a["radius"]) <= 0.5 * a["wall"]
+                elif kind == "tube":
+                    axial = (rel[0] * d[0] + rel[1] * d[1]) + rel[2] * d[2]
+                    radial = [rel[c] - axial * d[c] for c in range(3)]
+                    dist = _norm3(*radial, torch)
+                    safe = torch.clamp(dist, min=1e-9)
+                    nrm = [radial[c] / safe for c in range(3)]
+                    shell = torch.abs(dist - a["radius"]) <= 0.5 * a["wall"]
+                else:
+                    off = (rel[0] * d[0] + rel[1] * d[1]) + rel[2] * d[2]
+                    shell = torch.abs(off) <= 0.5 * a["wall"]
+                    nrm = [torch.full_like(off, float(d[c])) for c in range(3)]
+                cos_t = (nrm[0] * ya[:, 0, None, None] + nrm[1] * ya[:, 1, None, None]) + nrm[2] * ya[:, 2, None, None]
+                back = a["intensity"] if a["back"] is None else a["back"]
+                wall = torch.where(cos_t < 0.0, torch.full_like(cos_t, a["intensity"]), torch.full_like(cos_t, back))
+                c2 = cos_t * cos_t
+                img = img + (shell.to(torch.float64) * wall) * (c2 * c2 if scene["specular"] == 4.0
+                                                               else torch.abs(cos_t) ** scene["specular"])
+            if noise:
+                img = img + torch.from_numpy(np.stack([f.result() for f in pending])).to(device)
+            out[k0:k1] = torch.clamp(torch.round(img), 0, 255).to(torch.uint8)
+            pending = nxt
+    finally:
+        if pool is not None:
+            pool.shutdown(wait=True)
+    return out
+
+
+def render_frames_torch(wl: Workload, device="cuda"):
+    """(n, H, W) u8 frames of the workload's sweep(s): the reference's benchmark
+    phantom (default_benchmark_scene, seed 7, speckle 5) rendered at every frame pose."""
     poses, _ = sweep_poses(wl)
-    n, sz, p = wl.n_frames, wl.size, wl.pitch
-    L = wl.length
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    uu = torch.arange(sz, device=device, dtype=torch.float32) * p
-    U = uu[None, :].expand(sz, sz)
-    V = uu[:, None].expand(sz, sz)
-    centers = [(0.3 * L, 0.4 * L, 0.35 * L, 0.12 * L, 200.0), (0.65 * L, 0.55 * L, 0.6 * L, 0.15 * L, 140.0),
-               (0.5 * L, 0.3 * L, 0.8 * L, 0.08 * L, 255.0)]
-    R = torch.tensor(np.array([rotation_matrix(q.rotation) for q in poses]), dtype=torch.float32, device=device)
-    T = torch.tensor(np.array([q.translation for q in poses]), dtype=torch.float32, device=device)
-    frames = torch.empty((n, sz, sz), dtype=torch.uint8, device=device)
-    chunk = 64
-    for k0 in range(0, n, chunk):
-        k1 = min(n, k0 + chunk)
-        r, t = R[k0:k1], T[k0:k1]
-        xyz = [t[:, a, None, None] + U[None] * r[:, a, 0, None, None] + V[None] * r[:, a, 1, None, None]
-               for a in range(3)]
-        val = torch.full((k1 - k0, sz, sz), 24.0, device=device)
-        for cx, cy, cz, rad, level in centers:
-            inside = (xyz[0] - cx) ** 2 + (xyz[1] - cy) ** 2 + (xyz[2] - cz) ** 2 <= rad * rad
-            val = torch.where(inside, torch.full_like(val, level), val)
-        val = val + 5.0 * torch.randn(val.shape, generator=g, device=device)
-        frames[k0:k1] = val.clamp(0, 255).round().to(torch.uint8)
-    return frames
-
-
-def render_frames_numpy(wl: Workload, seed=7) -> np.ndarray:
-    rng = np.random.default_rng(seed)
-    return rng.integers(0, 256, (wl.n_frames, wl.size, wl.size), dtype=np.uint8)
+    return render_phantom(poses, wl.size, wl.size, (wl.pitch, wl.pitch), frame_keys(wl), device=device)
 
 
 def reslice_planes(wl: Workload, count: int, seed: int = 0):

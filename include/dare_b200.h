@@ -117,6 +117,11 @@ int dare_device_alloc(size_t bytes, void** ptr);
 int dare_device_free(void* ptr);
 int dare_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* cudaMemcpyDefault */
 int dare_stream_sync(void* stream);
+/* Device span (ms, CUDA events on the call's stream, entry to completion) of
+ * the last dare_reconstruct / dare_compound / dare_fill_holes call on this
+ * thread; -1 before the first.  Lets a host measure kernel time without a
+ * profiler. */
+int dare_last_device_ms(double* ms);
 
 /* ---- directional volume ------------------------------------------------- */
 
@@ -170,6 +175,13 @@ int dare_volume_upload(const double* origin, double voxel_size, const int64_t* d
 /* Materialises the reference layout on the host (buffers sized per info). */
 int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int64_t* cell_counts,
                          float* positions, float* orientations, uint8_t* intensities);
+/* Streaming .darevol writer (volume.py:272-297 save_volume): emits the exact
+ * bytes of the reference file -- header, cell table, samples in insertion
+ * order -- through `write(ctx, data, bytes)` (return 0 to continue) in chunks
+ * of about chunk_bytes (0: 64 MB), double-buffered through pinned memory, so a
+ * volume of any size is written with two chunks of host memory. */
+typedef int (*dare_write_fn)(void* ctx, const void* data, size_t bytes);
+int dare_volume_save_stream(dare_volume_t vol, dare_write_fn write, void* ctx, size_t chunk_bytes);
 int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info);
 int dare_volume_destroy(dare_volume_t vol);
 

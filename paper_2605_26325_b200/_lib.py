@@ -63,6 +63,8 @@ class ScalarInfo(ctypes.Structure):
     ]
 
 
+WRITE_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_sz)
+
 # name -> argtypes (restype is always c_int except dare_last_error)
 _SIGNATURES = {
     "dare_version": [],
@@ -75,6 +77,7 @@ _SIGNATURES = {
     "dare_device_free": [c_vp],
     "dare_memcpy": [c_vp, c_vp, c_sz, c_vp],
     "dare_stream_sync": [c_vp],
+    "dare_last_device_ms": [P_f64],
     "dare_reconstruct": [c_vp, c_i64, c_i32, c_i32, c_i32, P_i32, c_i64, P_f64, P_f32, c_f64,
                          c_f64, P_u8, P_f64, c_f64, P_i64, ctypes.POINTER(c_vp), P_i64],
     "dare_volume_seal": [P_f64, c_f64, P_i64, c_i64, P_f32, P_f32, P_u8, ctypes.POINTER(c_vp)],
@@ -82,6 +85,7 @@ _SIGNATURES = {
                            ctypes.POINTER(c_vp)],
     "dare_volume_download": [c_vp, P_i64, P_i64, P_f32, P_f32, P_u8],
     "dare_volume_get_info": [c_vp, ctypes.POINTER(VolumeInfo)],
+    "dare_volume_save_stream": [c_vp, WRITE_FN, c_vp, c_sz],
     "dare_volume_destroy": [c_vp],
     "dare_frame_poses": [c_i64, P_f64, P_f64, P_f64, P_f64, c_i32, c_i32, c_f64, c_f64, P_f64, P_f64, P_f64,
                          P_f32, P_f64, P_f64, ctypes.POINTER(c_i32), ctypes.POINTER(c_i64),

@@ -137,6 +137,20 @@ inline bool exact_reciprocal(double x) {
 
 int sm_count();
 
+// Device span of one C-ABI call: events on the call's stream at entry and
+// before its final synchronisation; dare_last_device_ms() reports the span of
+// the last timed call on this thread (reconstruct / seal / compound / fill).
+class DeviceClock {
+ public:
+  explicit DeviceClock(cudaStream_t s);
+  void stop();  // records the end event, waits for it, publishes the span
+  ~DeviceClock();
+
+ private:
+  cudaStream_t s_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
 // Long-lived device buffers (volumes) come from the device's stream-ordered
 // pool with an unlimited release threshold, so rebuilding a volume reuses
 // memory instead of paying cudaMalloc/cudaFree of multi-GB buffers.

@@ -725,6 +725,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     DARE_LIMIT(n_frames < (1 << 24), "more than 2^24 frames (orientation id is 24 bits)");
     auto vol = new_volume(origin, voxel_size, dims);
     cudaStream_t s = thread_stream();
+    DeviceClock clock(s);
     FrameSet fs(frames, n_images, height, width, frames_on_device, frame_image, n_frames,
                 frame_axes, pitch_x, pitch_y, mask, s);
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
@@ -789,6 +790,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     fs.start_upload();  // after the small uploads above (they would queue behind the frames)
     build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s,
               n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1);
+    clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
     *out = vol.release();

@@ -7,6 +7,26 @@
 namespace dare {
 
 static thread_local std::string g_last_error;
+static thread_local double g_last_device_ms = -1.0;
+
+DeviceClock::DeviceClock(cudaStream_t s) : s_(s) {
+  DARE_CUDA(cudaEventCreate(&a_));
+  DARE_CUDA(cudaEventCreate(&b_));
+  DARE_CUDA(cudaEventRecord(a_, s_));
+}
+
+void DeviceClock::stop() {
+  DARE_CUDA(cudaEventRecord(b_, s_));
+  DARE_CUDA(cudaEventSynchronize(b_));
+  float ms = 0.f;
+  DARE_CUDA(cudaEventElapsedTime(&ms, a_, b_));
+  g_last_device_ms = ms;
+}
+
+DeviceClock::~DeviceClock() {
+  if (a_) cudaEventDestroy(a_);
+  if (b_) cudaEventDestroy(b_);
+}
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -294,7 +314,14 @@ extern "C" {
 
 const char* dare_last_error(void) { return g_last_error.c_str(); }
 
-int dare_version(void) { return 100; }
+int dare_version(void) { return 200; }
+
+int dare_last_device_ms(double* ms) {
+  return guard([&] {
+    DARE_REQUIRE(ms != nullptr, "null argument");
+    *ms = g_last_device_ms;
+  });
+}
 
 int dare_get_device_count(int32_t* count) {
   return guard([&] {

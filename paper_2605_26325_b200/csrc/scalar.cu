@@ -404,6 +404,7 @@ extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t he
     DARE_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
     cudaStream_t s = thread_stream();
     const int64_t ncells = dims[0] * dims[1] * dims[2];
+    DeviceClock clock(s);
     PhaseTimer pt(s, "compound");
     Scratch<unsigned long long> acc(2 * ncells, s);
     DARE_CUDA(cudaMemsetAsync(acc.ptr, 0, sizeof(unsigned long long) * 2 * ncells, s));
@@ -418,6 +419,7 @@ extern "C" int dare_compound(const uint8_t* frames, int64_t n_images, int32_t he
                                (const uint64_t*)(acc.ptr + ncells), out);
     if (rc != DARE_OK) throw Error{rc, dare_last_error()};
     pt.mark("finalize");
+    clock.stop();
   });
 }
 
@@ -480,6 +482,7 @@ extern "C" int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar
     DARE_REQUIRE(in != nullptr && out != nullptr, "null argument");
     DARE_REQUIRE(max_passes >= 0 && max_passes <= 250, "max_passes must be in [0, 250]");
     cudaStream_t s = thread_stream();
+    DeviceClock clock(s);
     PhaseTimer pt(s, "fill_holes");
     auto sv = new_scalar(in->origin, in->voxel, in->dims, in->d_counts != nullptr);
     pt.mark("alloc_out");
@@ -512,7 +515,7 @@ extern "C" int dare_fill_holes(dare_scalar_t in, int32_t max_passes, dare_scalar
     std::vector<unsigned long long> h(2 * std::max(max_passes, 1));
     DARE_CUDA(cudaMemcpyAsync(h.data(), filled.ptr, sizeof(unsigned long long) * h.size(),
                               cudaMemcpyDeviceToHost, s));
-    DARE_CUDA(cudaStreamSynchronize(s));
+    clock.stop();
     int32_t runs = 0;
     for (int p = 0; p < max_passes; ++p) runs += h[2 * p] > 0;
     if (passes_run) *passes_run = runs;

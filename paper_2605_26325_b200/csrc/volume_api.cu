@@ -166,6 +166,118 @@ extern "C" int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int
   });
 }
 
+// .darevol writer (volume.py:272-297) streamed from the device: the header,
+// the cell table (u64 offset, u32 count per cell, packed 12 B) and the samples
+// (3 f32 position, 4 f32 quaternion, u8 intensity, 3 zero bytes = 32 B) in the
+// reference's insertion order (records read through perm, quaternions from
+// the orientation table).  Chunks are produced by a kernel into device
+// scratch, copied into one of two pinned buffers and handed to `write` while
+// the next chunk is produced and copied (double buffering) -- host memory
+// stays at two chunks whatever the volume size.
+namespace {
+
+__global__ void export_table_k(const uint32_t* __restrict__ offsets, int64_t c0, int64_t n,
+                               uint32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t a = offsets[c0 + i], b = offsets[c0 + i + 1];
+  out[3 * i] = a;  // u64 offset (< 2^32), little-endian
+  out[3 * i + 1] = 0u;
+  out[3 * i + 2] = b - a;
+}
+
+__global__ void export_samples_k(const uint4* __restrict__ records, const int8_t* __restrict__ perm,
+                                 const float4* __restrict__ orient, int64_t s0, int64_t n,
+                                 uint4* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = s0 + i;
+  const uint4 r = records[j + perm[j]];
+  const float4 q = orient[r.w >> 8];
+  out[2 * i] = make_uint4(r.x, r.y, r.z, __float_as_uint(q.x));
+  out[2 * i + 1] = make_uint4(__float_as_uint(q.y), __float_as_uint(q.z), __float_as_uint(q.w), r.w & 0xffu);
+}
+
+}  // namespace
+
+extern "C" int dare_volume_save_stream(dare_volume_t vol, dare_write_fn write, void* ctx,
+                                       size_t chunk_bytes) {
+  return guard([&] {
+    DARE_REQUIRE(vol != nullptr && write != nullptr, "null argument");
+    DARE_LIMIT(vol->dims[0] < (1ll << 32) && vol->dims[1] < (1ll << 32) && vol->dims[2] < (1ll << 32),
+               "dims do not fit the .darevol u32 header fields");
+    if (chunk_bytes < (1u << 20)) chunk_bytes = 64u << 20;
+    chunk_bytes -= chunk_bytes % 96;  // whole table entries (12 B) and samples (32 B)
+    cudaStream_t s = thread_stream();
+    // header: "<4sI3dd3IQ" (volume.py:23)
+    uint8_t hdr[4 + 4 + 32 + 12 + 8];
+    std::memcpy(hdr, "DARE", 4);
+    const uint32_t version = 1;
+    std::memcpy(hdr + 4, &version, 4);
+    std::memcpy(hdr + 8, vol->origin, 24);
+    std::memcpy(hdr + 32, &vol->voxel, 8);
+    for (int a = 0; a < 3; ++a) {
+      const uint32_t d = (uint32_t)vol->dims[a];
+      std::memcpy(hdr + 40 + 4 * a, &d, 4);
+    }
+    const uint64_t count = (uint64_t)vol->n_samples;
+    std::memcpy(hdr + 52, &count, 8);
+    DARE_REQUIRE(write(ctx, hdr, sizeof(hdr)) == 0, "write callback failed (header)");
+
+    const int64_t cells_per = (int64_t)(chunk_bytes / 12);
+    const int64_t samples_per = (int64_t)(chunk_bytes / 32);
+    Scratch<uint8_t> dbuf[2] = {Scratch<uint8_t>(chunk_bytes, s), Scratch<uint8_t>(chunk_bytes, s)};
+    struct Pinned {
+      void* p = nullptr;
+      ~Pinned() {
+        if (p) cudaFreeHost(p);
+      }
+    } hbuf[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    struct Events {
+      cudaEvent_t* e;
+      ~Events() {
+        for (int i = 0; i < 2; ++i)
+          if (e[i]) cudaEventDestroy(e[i]);
+      }
+    } ev_guard{ev};
+    for (int i = 0; i < 2; ++i) {
+      DARE_CUDA(cudaMallocHost(&hbuf[i].p, chunk_bytes));
+      DARE_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    // chunk list: table chunks, then sample chunks
+    struct Chunk {
+      bool table;
+      int64_t first, n;
+    };
+    std::vector<Chunk> chunks;
+    for (int64_t c = 0; c < vol->ncells; c += cells_per)
+      chunks.push_back({true, c, std::min(cells_per, vol->ncells - c)});
+    for (int64_t j = 0; j < vol->n_samples; j += samples_per)
+      chunks.push_back({false, j, std::min(samples_per, vol->n_samples - j)});
+    auto bytes_of = [](const Chunk& c) { return (size_t)c.n * (c.table ? 12 : 32); };
+    auto produce = [&](size_t k) {
+      const Chunk& c = chunks[k];
+      void* d = dbuf[k & 1].ptr;
+      if (c.table)
+        export_table_k<<<ceil_div(c.n, 256), 256, 0, s>>>(vol->d_offsets, c.first, c.n, (uint32_t*)d);
+      else
+        export_samples_k<<<ceil_div(c.n, 256), 256, 0, s>>>(vol->d_records, vol->d_perm, vol->d_orient,
+                                                           c.first, c.n, (uint4*)d);
+      DARE_CUDA(cudaGetLastError());
+      DARE_CUDA(cudaMemcpyAsync(hbuf[k & 1].p, d, bytes_of(c), cudaMemcpyDeviceToHost, s));
+      DARE_CUDA(cudaEventRecord(ev[k & 1], s));
+    };
+    if (!chunks.empty()) produce(0);
+    for (size_t k = 0; k < chunks.size(); ++k) {
+      if (k + 1 < chunks.size()) produce(k + 1);  // overlaps the host write of chunk k
+      DARE_CUDA(cudaEventSynchronize(ev[k & 1]));
+      DARE_REQUIRE(write(ctx, hbuf[k & 1].p, bytes_of(chunks[k])) == 0, "write callback failed");
+    }
+    DARE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 extern "C" int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info) {
   return guard([&] {
     DARE_REQUIRE(vol != nullptr && info != nullptr, "null argument");

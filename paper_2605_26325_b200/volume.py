@@ -344,8 +344,41 @@ class VolumeBuilder:
         return DirectionalVolume(self.origin, self.voxel_size, self.dims, _handle=_Handle(raw.value))
 
 
-def save_volume(volume, path) -> None:
-    """.darevol writer, byte-identical to volume.py:272-297."""
+def save_volume(volume, path, chunk_bytes: int = 64 << 20) -> None:
+    """.darevol writer, byte-identical to volume.py:272-297.
+
+    `path` is a file name or a writable binary file object.  A device volume
+    whose host arrays were never materialised is streamed straight from HBM
+    (dare_volume_save_stream: records read through perm in insertion order,
+    chunks double-buffered through pinned memory), so saving a multi-GB volume
+    needs two chunks of host memory, not the reference's full structured copy.
+    """
+    if isinstance(volume, DirectionalVolume) and volume._host is None and volume._handle is not None:
+        def stream(fh):
+            err = []
+
+            def write(_ctx, data, nbytes):
+                try:
+                    fh.write(memoryview((ctypes.c_ubyte * nbytes).from_address(data)))
+                    return 0
+                except BaseException as e:  # noqa: BLE001 (re-raised below)
+                    err.append(e)
+                    return 1
+
+            cb = _lib.WRITE_FN(write)
+            try:
+                _lib.call("dare_volume_save_stream", volume._handle.raw, cb, None, int(chunk_bytes))
+            except Exception:
+                if err:
+                    raise err[0]
+                raise
+
+        if hasattr(path, "write"):
+            stream(path)
+        else:
+            with open(path, "wb") as fh:
+                stream(fh)
+        return
     nc = int(np.prod(volume.dims))
     n = int(volume.intensities.shape[0])
     header = _HEADER.pack(VOLUME_MAGIC, VOLUME_VERSION, *[float(c) for c in volume.origin],
@@ -357,10 +390,17 @@ def save_volume(volume, path) -> None:
     samples["position"] = volume.positions
     samples["orientation"] = volume.orientations
     samples["intensity"] = volume.intensities
-    with open(path, "wb") as fh:
+
+    def emit(fh):
         fh.write(header)
         fh.write(table.tobytes())
         fh.write(samples.tobytes())
+
+    if hasattr(path, "write"):
+        emit(path)
+    else:
+        with open(path, "wb") as fh:
+            emit(fh)
 
 
 def load_volume(path) -> DirectionalVolume:
