@@ -184,6 +184,67 @@ def ncu_traffic(kernel: str, batch: int, config: str):
         return None, f"no ncu capture ({type(e).__name__})"
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def host_cores() -> dict:
+    n = os.cpu_count() or 1
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = n
+    return {"cpu_count": n, "affinity": avail, "model": cpu_model()}
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1, devices checked by main) without a torchrun
+    environment: relaunch this script under torch.distributed.run with N ranks
+    on 127.0.0.1 (NCCL_DEBUG=INFO, so every rank's communicator is logged)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def last_device_ms() -> float:
+    """Device span (CUDA events on the library's stream) of this thread's last
+    reconstruct / compound / fill_holes C-ABI call."""
+    from paper_2605_26325_b200 import _lib
+
+    ms = ctypes.c_double(-1.0)
+    _lib.call("dare_last_device_ms", ctypes.byref(ms))
+    return float(ms.value)
+
+
+def recon_traffic(config: str):
+    """ncu DRAM bytes (read + write) of one reconstruction's kernels, from the
+    committed capture (profiles/round2_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2_traffic.json")) as fh:
+            data = json.load(fh)
+        rec = data.get("recon", {}).get(config)
+        return (float(rec["dram_bytes"]), "profiles/round2_traffic.json (" + data["source"] + ")") if rec else \
+            (None, f"no ncu capture of the {config} reconstruction")
+    except Exception as e:  # noqa: BLE001
+        return None, f"no ncu capture ({type(e).__name__})"
+
+
 def make_rank_info():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -249,23 +310,40 @@ class OracleSlab:
         return (time.perf_counter() - t0) * 1000.0, px, cov, nf
 
 
-def oracle_sample(wl, sweep, plane_list, cfg, gpu=None, patch=None):
-    """CPU oracle (C + OpenMP, all host cores) on a bounded sample of poses.
-    Returns (ms per full-plane reslice for each pose, parity flags, description)."""
+def oracle_baseline(wl, sweep, plane, cfg, gpu_px=None, gpu_cov=None, reps: int = 3):
+    """CPU oracle (C; reslice rows in parallel with OpenMP over the host cores
+    like the reference's thread pool, reconstruction single-threaded like the
+    reference's numpy loop) on a bounded sample of the workload: the slab of
+    frames that can reach `plane` is reconstructed into the full
+    grid (timed: recon Mpix/s), then the full plane is resliced once untimed
+    (warm-up) and `reps` times timed (reslices/s).  Bit-exact parity of the
+    oracle pixels with the GPU's is reported."""
     slab = OracleSlab(wl, sweep)
-    times, parity = [], []
-    for plane in plane_list:
-        sp = patch_plane(plane, patch) if patch else plane
-        ms, px, cov, nf = slab.reslice(sp, cfg)
-        scale = (plane.width * plane.height) / (sp.width * sp.height)
-        times.append(ms * scale)
-        if gpu is not None:
-            gp, gc = gpu(sp)
-            parity.append(bool(np.array_equal(px, gp) and np.array_equal(cov, gc)))
-    what = (f"{len(plane_list)} reslices of {'a ' + str(patch) + 'x' + str(patch) + ' centre patch of ' if patch else ''}"
-            f"{plane_list[0].width}x{plane_list[0].height} planes on a slab-oracle volume (frames within one "
-            f"voxel of the plane, full grid){', time scaled by pixel count' if patch else ''}; C+OpenMP")
-    return times, parity, what
+    t0 = time.perf_counter()
+    vol, nf = slab.volume_for(plane, cfg.interp_radius)
+    t_rec = time.perf_counter() - t0
+    p = slab.o.plane_params(plane)
+    c = slab.o.cfg_array(cfg)
+    slab.o.reslice(vol, p, c, plane.width, plane.height, cfg.unassigned_value)  # warm-up
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        px, cov = slab.o.reslice(vol, p, c, plane.width, plane.height, cfg.unassigned_value)
+        times.append(time.perf_counter() - t0)
+    hc = host_cores()
+    parity = None if gpu_px is None else bool(np.array_equal(px, gpu_px) and np.array_equal(cov, gpu_cov))
+    ms = 1000.0 * statistics.median(times)
+    reslice = {"value": 1000.0 / ms, "unit": "reslices/s", "cores": hc["affinity"], "kind": "port",
+               "cpu": hc["model"], "ms_per_reslice": ms,
+               "sample": f"{reps} timed full {plane.width}x{plane.height} reslices (median; 1 untimed warm-up) on a "
+                         f"slab-oracle volume ({nf} frames that reach the plane, full grid); C + OpenMP over "
+                         f"{hc['affinity']} host threads",
+               "parity_with_gpu": parity}
+    npx = nf * wl.size * wl.size
+    recon = {"value": npx / 1e6 / t_rec, "unit": "Mpix/s", "cores": 1, "kind": "port", "cpu": hc["model"],
+             "sample": f"oracle reconstruct of {nf} frames ({npx} pixels) into the full grid (frame_cells + "
+                       f"stable seal, single-threaded C), {t_rec:.2f} s"}
+    return reslice, recon
 
 
 def _best_ms(fn, reps=3):
@@ -381,53 +459,81 @@ def host_sweep(wl, frames_np):
                            pixel_pitch=(wl.pitch, wl.pitch), calibration=Pose.identity(), mask=None)
 
 
+def bench_frames(wl):
+    """The workload's frames (the reference's benchmark phantom, bench_data):
+    rendered on the GPU when one is visible (setup only), else on the CPU."""
+    import torch
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    return bench_data.render_frames_torch(wl, device=dev).cpu().numpy()
+
+
 def run_reference(args):
-    """Reference arm: the reference's CPU algorithm (oracle port) on this box's host cores."""
+    """Reference arm: the reference's CPU algorithm (the oracle port, C + OpenMP;
+    the reference itself is pure Python/numba and is not on the GPU box) on this
+    box's host cores, same config, frames and planes as the B200 arm.  Single-
+    sweep configs: the full volume is reconstructed once (timed: recon Mpix/s,
+    single-threaded like the reference's numpy loop), then every step reslices
+    one full plane (rows in parallel over all host threads, like the reference's
+    pool).  Multi-sweep configs (cfg3/cfg4 need ~300 GB on the host): slab
+    volumes of 64x64 centre patches, time scaled by pixel count."""
     ws, rank, _ = make_rank_info()
     if rank != 0:
         return
+    from oracle import oracle
+
     from paper_2605_26325_b200.reslice import ResliceConfig
 
     wl = bench_data.workload(args.config)
-    frames_np = bench_data.render_frames_numpy(wl)
-    sweep = host_sweep(wl, frames_np)
+    sweep = host_sweep(wl, bench_frames(wl))
     cfg = ResliceConfig(interp_radius=wl.voxel)
     planes = bench_data.reslice_planes(wl, args.warmup + args.steps)
-    # bounded: slab volumes for at most 4 distinct poses (64x64 centre patches of
-    # planes larger than 128x128), then K timed reslices cycling over them
-    patch = 64 if wl.plane > 128 else None
-    slab = OracleSlab(wl, sweep)
-    distinct = [patch_plane(p, patch) if patch else p for p in planes[args.warmup: args.warmup + 4]]
-    vols = [slab.volume_for(p, cfg.interp_radius)[0] for p in distinct]
-    cfga = slab.o.cfg_array(cfg)
-    scale = (planes[0].width * planes[0].height) / (distinct[0].width * distinct[0].height)
-    for i in range(args.warmup):
-        sp = distinct[i % len(distinct)]
-        slab.o.reslice(vols[i % len(distinct)], slab.o.plane_params(sp), cfga, sp.width, sp.height)
-    times = []
-    for i in range(args.steps):
-        sp, vol = distinct[i % len(distinct)], vols[i % len(distinct)]
-        pp = slab.o.plane_params(sp)
+    cfga = oracle.cfg_array(cfg)
+    hc = host_cores()
+    recon = None
+    if wl.sweeps == 1:
         t0 = time.perf_counter()
-        slab.o.reslice(vol, pp, cfga, sp.width, sp.height)
-        times.append((time.perf_counter() - t0) * 1000.0 * scale)
-    what = (f"{args.steps} reslices cycling over {len(distinct)} poses"
-            f"{' (' + str(patch) + 'x' + str(patch) + ' centre patches, time scaled by pixel count)' if patch else ''}"
-            f" of {planes[0].width}x{planes[0].height} planes on slab-oracle volumes (frames within one voxel of"
-            f" the plane, full grid); C+OpenMP on all host cores")
+        vol = oracle.reconstruct(sweep, wl.voxel, 0.0)
+        t_rec = time.perf_counter() - t0
+        npx = wl.n_frames * wl.size * wl.size
+        recon = {"value": npx / 1e6 / t_rec, "unit": "Mpix/s", "ms": 1000.0 * t_rec, "cores": 1,
+                 "sample": f"full reconstruct_volume of the workload ({npx} pixels -> dims {tuple(vol.dims)})"}
+        jobs = [(p, vol, 1.0) for p in planes]
+        what = (f"full {wl.plane}x{wl.plane} planes on the full {tuple(vol.dims)} oracle volume (built once, "
+                f"timed separately as recon)")
+    else:
+        patch = 64
+        slab = OracleSlab(wl, sweep)
+        distinct = [patch_plane(p, patch) for p in planes[args.warmup: args.warmup + 2]]
+        vols = [slab.volume_for(p, cfg.interp_radius)[0] for p in distinct]
+        scale = (wl.plane * wl.plane) / (patch * patch)
+        jobs = [(distinct[i % 2], vols[i % 2], scale) for i in range(args.warmup + args.steps)]
+        what = (f"{patch}x{patch} centre patches of {wl.plane}x{wl.plane} planes (cycling over 2 poses, time "
+                f"scaled by pixel count) on slab-oracle volumes (frames that reach the patch, full grid)")
+    for i in range(args.warmup):
+        p, v, _ = jobs[i]
+        oracle.reslice(v, oracle.plane_params(p), cfga, p.width, p.height, cfg.unassigned_value)
+    times = []
+    for i in range(args.warmup, args.warmup + args.steps):
+        p, v, sc = jobs[i]
+        pp = oracle.plane_params(p)
+        t0 = time.perf_counter()
+        oracle.reslice(v, pp, cfga, p.width, p.height, cfg.unassigned_value)
+        times.append((time.perf_counter() - t0) * 1000.0 * sc)
     ms = statistics.mean(times)
     value = 1000.0 / ms
-    cores = os.cpu_count()
     out = {
         "impl": "reference", "metric": "reslices/sec", "value": value, "unit": "reslices/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "p50_reslice_ms": statistics.median(times),
+        "data": "synthetic (the reference's benchmark phantom at the workload's sweep poses, as the B200 arm)",
+        "p50_reslice_ms": statistics.median(times),
         "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> "
                                f"{wl.voxel} mm grid, 1 pose/step at {wl.plane}x{wl.plane}",
-                   "parallelism": "host threads (OpenMP)"},
-        "cpu_baseline": {"value": value, "unit": "reslices/s", "cores": cores, "kind": "port",
-                         "sample": what + " (slab reconstruct untimed)"},
+                   "parallelism": f"host threads (OpenMP, {hc['affinity']})"},
+        "cpu_baseline": {"value": value, "unit": "reslices/s", "cores": hc["affinity"], "kind": "port",
+                         "cpu": hc["model"], "sample": f"{args.steps} reslices: {what}; C + OpenMP"},
+        "recon": recon,
         "e2e": {"value": value, "unit": "reslices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -443,12 +549,17 @@ def run_b200(args):
     from paper_2605_26325_b200.reslice import ResliceConfig, kernel_cfg, plane_params
 
     ws, rank, local = make_rank_info()
+    if torch.cuda.device_count() <= local:
+        sys.stderr.write(f"bench.py: rank {rank} needs CUDA device {local} but only "
+                         f"{torch.cuda.device_count()} are visible; refusing to run\n")
+        sys.exit(2)
     torch.cuda.set_device(local)
     _lib.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
@@ -479,7 +590,7 @@ def run_b200(args):
                                 pixel_pitch=(wl.pitch, wl.pitch), calibration=Pose.identity(), mask=None)
     npix = wl.n_frames * wl.size * wl.size
     db.reconstruct_volume(dev_sweep, voxel_size=wl.voxel, margin=0.0)  # warm-up (allocator pools, modules)
-    recon_ms = []
+    recon_ms, recon_span = [], []
     vol = None
     for _ in range(3):
         del vol
@@ -487,7 +598,10 @@ def run_b200(args):
         t0 = time.perf_counter()
         vol = db.reconstruct_volume(dev_sweep, voxel_size=wl.voxel, margin=0.0)
         recon_ms.append((time.perf_counter() - t0) * 1000.0)
-    recon_dev_ms = max_over_ranks(min(recon_ms))
+        recon_span.append(last_device_ms())
+    best = int(np.argmin(recon_ms))
+    recon_dev_ms = max_over_ranks(recon_ms[best])
+    recon_span_ms = max_over_ranks(recon_span[best])
     frames_pinned = frames_d.cpu().pin_memory()
     frames_np = frames_pinned.numpy()
     host_sw = host_sweep(wl, frames_np)
@@ -653,26 +767,31 @@ def run_b200(args):
         scalar_arm = scalar_arm_bench(db, wl, dev_sweep, frames_d, planes[step0 * B:(step0 + 1) * B], peak, torch)
 
     # ---- CPU baseline (rank 0, bounded sample) ----
-    cpu = None
+    cpu = recon_cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        sample_planes = planes[step0 * B: step0 * B + 2]
-
-        def gpu_one(sp):
-            gp, gc, _ = db.reslice_batch(vol, [sp], cfg)
-            return gp[0], gc[0]
-
-        t_ms, parity, what = oracle_sample(wl, host_sw, sample_planes, cfg, gpu=gpu_one,
-                                           patch=64 if wl.plane > 128 else None)
-        cpu = {"value": 1000.0 / statistics.mean(t_ms), "unit": "reslices/s", "cores": os.cpu_count(),
-               "kind": "port", "sample": what,
-               "parity_with_gpu": all(parity)}
+        plane0 = planes[step0 * B]
+        gp, gc, _ = db.reslice_batch(vol, [plane0], cfg)
+        cpu, recon_cpu = oracle_baseline(wl, host_sw, plane0, cfg, gp[0], gc[0])
+    ncells_total = int(np.prod(dims))
+    recon_alg = npix * 1 + 29 * int(info.n_samples) + 12 * ncells_total
+    r_traffic, r_traffic_src = recon_traffic(args.config)
+    recon_roof = {
+        "bound": "hbm", "algorithmic_bytes": recon_alg,
+        "formula": "N_in*1 + N_samples*29 + ncells*12 (SURVEY 8d, reference layout)",
+        "achieved_device": recon_alg / (recon_span_ms / 1000.0) / 1e9,
+        "frac_device": recon_alg / (recon_span_ms / 1000.0) / 1e9 / peak,
+        "achieved_wall": recon_alg / (recon_dev_ms / 1000.0) / 1e9,
+        "frac_wall": recon_alg / (recon_dev_ms / 1000.0) / 1e9 / peak,
+        "peak": peak, "unit": "GB/s", "traffic": r_traffic, "traffic_source": r_traffic_src,
+        "note": "device = CUDA-event span of the dare_reconstruct call on its stream (first kernel to seal); "
+                "wall = the Python reconstruct_volume call incl. host pose pipeline and syncs"}
 
     if rank == 0:
         out = {
             "metric": "reslices/sec", "value": value, "unit": "reslices/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if args.exact else "f32 weights + f64 sums (certified, exact u8 output)",
-            "data": "synthetic",
+            "data": "synthetic (the reference's benchmark phantom rendered at the workload's sweep poses)",
             "config": {"workload": f"{args.config}: {wl.n_frames} frames {wl.size}x{wl.size} -> dims {dims} "
                                    f"({info.n_samples} samples), {B} poses/step at {W}x{H}, r={cfg.interp_radius}",
                        "poses_per_step": B, "parallelism": f"pose-sharded x{ws} (replicated volume)",
@@ -682,12 +801,14 @@ def run_b200(args):
                              f"{own_bytes / 1e9:.2f} GB)"},
             "p50_reslice_ms": p50, "p95_reslice_ms": p95,
             "recon": {"metric": "recon input Mpix/s", "value": ws * npix / 1e6 / (recon_dev_ms / 1000.0),
-                      "ms": recon_dev_ms, "e2e_value": ws * npix / 1e6 / (recon_e2e_ms / 1000.0),
+                      "ms": recon_dev_ms, "device_ms": recon_span_ms,
+                      "device_value": ws * npix / 1e6 / (recon_span_ms / 1000.0),
+                      "e2e_value": ws * npix / 1e6 / (recon_e2e_ms / 1000.0),
                       "e2e_ms": recon_e2e_ms, "input_pixels": npix, "samples": int(info.n_samples),
                       "frame_sharded_ms": sharded_ms, "frame_sharded_error": sharded_err,
-                      "note": "wall time of the C-ABI call (frames in HBM / from pinned host), incl. host syncs"},
-            "e2e_2threads": {"value": e2e2_value, "unit": "reslices/s",
-                             "note": "the e2e calls issued from two host threads (re-entrant API)"},
+                      "roofline": recon_roof, "cpu_baseline": recon_cpu,
+                      "note": "value/ms = wall time of reconstruct_volume with frames in HBM (host pose pipeline + "
+                              "C-ABI call incl. syncs); e2e = the same from pinned host frames (PCIe upload inside)"},
             "e2e_2threads": {"value": e2e2_value, "unit": "reslices/s",
                              "note": "the e2e calls issued from two host threads (re-entrant API)"},
             "e2e": {"value": e2e_value, "unit": "reslices/s", "h2d_bytes_per_step": B * 14 * 8,
@@ -712,10 +833,24 @@ def run_b200(args):
 
 def main():
     args = parse_args()
+    ws_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_b200(args)
+        return
+    if ws_env is None:
+        import torch
+
+        n_dev = torch.cuda.device_count()
+        if n_dev < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {n_dev} CUDA device(s) are visible; "
+                             f"refusing to run {args.gpus} ranks on fewer GPUs\n")
+            sys.exit(2)
+        if args.gpus > 1:
+            sys.exit(spawn_ranks(args))
+    if ws_env is not None and int(ws_env) != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}\n")
+        sys.exit(2)
+    run_b200(args)
 
 
 if __name__ == "__main__":

@@ -117,6 +117,16 @@ int dare_device_alloc(size_t bytes, void** ptr);
 int dare_device_free(void* ptr);
 int dare_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* cudaMemcpyDefault */
 int dare_stream_sync(void* stream);
+/* Start-up for a process / service: makes `device` current, creates the
+ * calling thread's stream and runs the one-time exhaustive check of the
+ * hardware ex2/sqrt approximations that the certified reslice path relies on
+ * (dare_fastmath_check), so the first reslice request does not pay it. */
+int dare_init(int32_t device);
+/* Returns unused memory of the current device's stream-ordered pool (volumes
+ * and build scratch come from it; its release threshold is unlimited so that
+ * rebuilds reuse memory) to the driver, keeping at most keep_bytes reserved.
+ * Synchronises the device. */
+int dare_trim(size_t keep_bytes);
 /* Device span (ms, CUDA events on the call's stream, entry to completion) of
  * the last dare_reconstruct / dare_compound / dare_fill_holes call on this
  * thread; -1 before the first.  Lets a host measure kernel time without a

@@ -78,6 +78,8 @@ _SIGNATURES = {
     "dare_memcpy": [c_vp, c_vp, c_sz, c_vp],
     "dare_stream_sync": [c_vp],
     "dare_last_device_ms": [P_f64],
+    "dare_init": [c_i32],
+    "dare_trim": [c_sz],
     "dare_reconstruct": [c_vp, c_i64, c_i32, c_i32, c_i32, P_i32, c_i64, P_f64, P_f32, c_f64,
                          c_f64, P_u8, P_f64, c_f64, P_i64, ctypes.POINTER(c_vp), P_i64],
     "dare_volume_seal": [P_f64, c_f64, P_i64, c_i64, P_f32, P_f32, P_u8, ctypes.POINTER(c_vp)],
@@ -187,3 +189,13 @@ def device_count() -> int:
 
 def set_device(dev: int) -> None:
     call("dare_set_device", int(dev))
+
+
+def init(dev: int = 0) -> None:
+    """dare_init: device, stream and the one-time fast-math check up front."""
+    call("dare_init", int(dev))
+
+
+def trim(keep_bytes: int = 0) -> None:
+    """dare_trim: release unused pooled device memory (volumes / build scratch)."""
+    call("dare_trim", int(keep_bytes))

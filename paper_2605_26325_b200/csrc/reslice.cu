@@ -1417,6 +1417,18 @@ extern "C" int dare_reslice_last_fallback(int64_t* n_pixels) {
   });
 }
 
+// Process / service start-up: makes `device` current, creates the calling
+// thread's stream (and the device pool settings), and runs the one-time
+// exhaustive ex2/sqrt check the certified reslice path depends on, so the
+// first request does not pay it (~14 ms at first use otherwise).
+extern "C" int dare_init(int32_t device) {
+  return guard([&] {
+    DARE_CUDA(cudaSetDevice(device));
+    cudaStream_t s = thread_stream();
+    (void)fastmath_ok(s);
+  });
+}
+
 extern "C" int dare_fastmath_check(double* ex2_max_rel_err, double* sqrt_max_rel_err, int32_t* ok) {
   return guard([&] {
     double e1 = 1.0, e2 = 1.0;

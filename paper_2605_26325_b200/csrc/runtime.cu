@@ -355,6 +355,17 @@ int dare_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
   });
 }
 
+int dare_trim(size_t keep_bytes) {
+  return guard([&] {
+    int dev = 0;
+    DARE_CUDA(cudaGetDevice(&dev));
+    DARE_CUDA(cudaDeviceSynchronize());  // pending frees of every stream complete
+    cudaMemPool_t pool;
+    DARE_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    DARE_CUDA(cudaMemPoolTrimTo(pool, keep_bytes));
+  });
+}
+
 int dare_stream_sync(void* stream) {
   return guard([&] {
     DARE_CUDA(cudaStreamSynchronize(stream ? (cudaStream_t)stream : thread_stream()));

@@ -191,6 +191,9 @@ class ResliceBatcher:
         # throughput (10k -> 7k requests/s), so the default is 1
         if int(workers) < 1:
             raise InvalidArgumentError("workers must be >= 1")
+        # device set-up and the one-time fast-math check now, not on the first request
+        dev = int(volume.device_info().device) if hasattr(volume, "device_info") else 0
+        _lib.init(dev)
         self._threads = [threading.Thread(target=self._loop, name=f"dare-batcher-{i}", daemon=True)
                          for i in range(int(workers))]
         for t in self._threads:
