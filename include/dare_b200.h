@@ -160,18 +160,20 @@ int dare_volume_seal(const double* origin, double voxel_size, const int64_t* dim
 
 /* Frame-sharded reconstruction (multi-GPU): merges n_parts partial
  * volumes built by dare_reconstruct over consecutive frame blocks into the
- * SAME grid.  Parts are given as device buffers on the current device (the
- * d_* views of dare_volume_info, or the same arrays received through NCCL):
- * per part the ncells+1 offsets, the 16 B records IN INSERTION ORDER (a
- * handle's d_records read through its d_perm), the orientation table and
- * its sizes.  Within each cell the parts' runs are concatenated in part
- * order, which is the reference's insertion order when part r holds frames
- * after part r-1 -- the result is bit-identical to a single-device build. */
+ * SAME grid.  Parts are device buffers on the current device (the d_* views
+ * of dare_volume_info, or the same arrays received through NCCL): per part
+ * the ncells+1 offsets, the 16 B records in the part's storage order with its
+ * perm (insertion order is read through it; NULL perm array or entry = records
+ * already in insertion order), the orientation table and its sizes.  Within
+ * each cell the parts' runs are concatenated in part order -- the reference's
+ * insertion order when part r holds frames after part r-1 -- and orientation
+ * tables are deduplicated in part order, so the result (records, orientation
+ * ids, bins, perm) is bit-identical to a single-device build. */
 int dare_volume_merge(const double* origin, double voxel_size, const int64_t* dims,
                       int32_t n_parts, const uint32_t* const* d_offsets,
-                      const void* const* d_records, const float* const* d_orient,
-                      const int64_t* n_samples, const int64_t* n_orient, const int64_t* rejected,
-                      dare_volume_t* out);
+                      const void* const* d_records, const int8_t* const* d_perm,
+                      const float* const* d_orient, const int64_t* n_samples,
+                      const int64_t* n_orient, const int64_t* rejected, dare_volume_t* out);
 
 /* Uploads a sealed volume in the reference layout (volume.py:76-93, as
  * produced by VolumeBuilder.seal or load_volume volume.py:300-330):
@@ -193,6 +195,8 @@ int dare_volume_download(dare_volume_t vol, int64_t* cell_starts, int64_t* cell_
 typedef int (*dare_write_fn)(void* ctx, const void* data, size_t bytes);
 int dare_volume_save_stream(dare_volume_t vol, dare_write_fn write, void* ctx, size_t chunk_bytes);
 int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info);
+/* Frees the volume after synchronising its device (so reslices still queued
+ * on caller streams by dare_reslice_device finish first). */
 int dare_volume_destroy(dare_volume_t vol);
 
 /* Replaces reslice.py:168-187 reslice -> _run_rows -> _kernels.reslice_rows_grid
@@ -264,7 +268,9 @@ int dare_compound_accumulate(const uint8_t* frames, int64_t n_images, int32_t he
                              uint64_t* d_counts, void* stream);
 int dare_scalar_from_sums(const double* origin, double voxel_size, const int64_t* dims,
                           const uint64_t* d_sums, const uint64_t* d_counts, dare_scalar_t* out);
-/* Uploads values f32 / flags u8 / counts i64 (counts may be NULL). */
+/* Creates a scalar volume from values f32 / flags u8 / counts i64 (counts may
+ * be NULL), host or device pointers (unified addressing: e.g. buffers received
+ * through an NCCL broadcast are copied device-to-device). */
 int dare_scalar_upload(const double* origin, double voxel_size, const int64_t* dims,
                        const float* values, const uint8_t* flags, const int64_t* counts,
                        dare_scalar_t* out);

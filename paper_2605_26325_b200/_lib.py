@@ -102,7 +102,7 @@ _SIGNATURES = {
     "dare_compound": [c_vp, c_i64, c_i32, c_i32, c_i32, P_i32, c_i64, P_f64, c_f64, c_f64, P_u8,
                       P_f64, c_f64, P_i64, ctypes.POINTER(c_vp)],
     "dare_volume_merge": [P_f64, c_f64, P_i64, c_i32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
-                          ctypes.POINTER(c_vp), P_i64, P_i64, P_i64, ctypes.POINTER(c_vp)],
+                          ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), P_i64, P_i64, P_i64, ctypes.POINTER(c_vp)],
     "dare_compound_accumulate": [c_vp, c_i64, c_i32, c_i32, c_i32, P_i32, c_i64, P_f64, c_f64, c_f64,
                                  P_u8, P_f64, c_f64, P_i64, c_vp, c_vp, c_vp],
     "dare_scalar_from_sums": [P_f64, c_f64, P_i64, c_vp, c_vp, ctypes.POINTER(c_vp)],

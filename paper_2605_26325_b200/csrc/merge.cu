@@ -8,10 +8,14 @@
 //   records   = per cell, the parts' runs concatenated in rank order, with the
 //               orientation id rebased into the concatenated orientation table.
 // The parts are device buffers on the calling device (the local volume plus
-// buffers received through NCCL all-gather, or several local partial volumes
-// when the ranks are emulated on one GPU in tests), records in insertion
-// order (a handle's storage order read through its perm); the merged volume is
-// z-binned like every other (volume.cuh).
+// buffers received through NCCL, or several local partial volumes when the
+// ranks are emulated on one GPU in tests): a part's records in its storage
+// order plus its perm (insertion order is read through perm, so no gathered
+// copy is ever made) or, with a null perm, already in insertion order.
+// Orientation tables are deduplicated in rank order (first occurrence wins,
+// = the single-device dedup order over frames), so the merged records,
+// orientation table, bins and perm equal a single-device build's exactly;
+// the merged volume is z-binned like every other (volume.cuh).
 #include <cub/device/device_scan.cuh>
 
 #include <memory>
@@ -23,8 +27,9 @@ namespace dare {
 
 struct MergeParts {
   const uint32_t* const* offsets;  // device array of n device pointers
-  const uint4* const* records;
-  const uint32_t* orient_base;     // rebasing offset per part
+  const uint4* const* records;     // storage order
+  const int8_t* const* perm;       // per part: insertion -> storage offset, or null
+  const uint32_t* const* remap;    // per part: local orientation id -> merged id
   int n;
 };
 
@@ -45,10 +50,11 @@ __global__ void merge_copy_k(MergeParts p, int64_t ncells, const uint32_t* __res
   uint32_t dst = out_off[c];
   for (int r = 0; r < p.n; ++r) {
     const uint32_t s = p.offsets[r][c], e = p.offsets[r][c + 1];
-    const uint32_t base = p.orient_base[r];
+    const int8_t* perm = p.perm[r];
+    const uint32_t* remap = p.remap[r];
     for (uint32_t j = s + lane; j < e; j += 32) {
-      uint4 rec = p.records[r][j];
-      rec.w = (((rec.w >> 8) + base) << 8) | (rec.w & 0xffu);
+      uint4 rec = p.records[r][perm ? canon_to_store(perm, j) : j];
+      rec.w = (__ldg(remap + (rec.w >> 8)) << 8) | (rec.w & 0xffu);
       out[dst + (j - s)] = rec;
     }
     dst += e - s;
@@ -61,19 +67,17 @@ using namespace dare;
 
 extern "C" int dare_volume_merge(const double* origin, double voxel_size, const int64_t* dims,
                                  int32_t n_parts, const uint32_t* const* d_offsets,
-                                 const void* const* d_records, const float* const* d_orient,
-                                 const int64_t* n_samples, const int64_t* n_orient,
-                                 const int64_t* rejected, dare_volume_t* out) {
+                                 const void* const* d_records, const int8_t* const* d_perm,
+                                 const float* const* d_orient, const int64_t* n_samples,
+                                 const int64_t* n_orient, const int64_t* rejected, dare_volume_t* out) {
   return guard([&] {
     DARE_REQUIRE(out != nullptr && n_parts >= 1, "need an output handle and at least one part");
     DARE_REQUIRE(voxel_size > 0, "voxel_size must be > 0");
     DARE_REQUIRE(dims[0] > 0 && dims[1] > 0 && dims[2] > 0, "dims must be positive");
     const int64_t ncells = dims[0] * dims[1] * dims[2];
     DARE_LIMIT(ncells < (int64_t)INT32_MAX, "more than 2^31 cells");
-    int64_t total = 0, total_orient = 0, total_rej = 0;
-    std::vector<uint32_t> orient_base(n_parts);
+    int64_t total = 0, total_rej = 0, total_orient = 0;
     for (int r = 0; r < n_parts; ++r) {
-      orient_base[r] = (uint32_t)total_orient;
       total += n_samples[r];
       total_orient += n_orient[r];
       total_rej += rejected ? rejected[r] : 0;
@@ -81,6 +85,26 @@ extern "C" int dare_volume_merge(const double* origin, double voxel_size, const 
     DARE_LIMIT(total < (int64_t)UINT32_MAX, "more than 2^32-1 samples");
     DARE_LIMIT(total_orient < (1 << 24), "more than 2^24 orientations");
     cudaStream_t s = thread_stream();
+    // orientation tables: rank-ordered first-occurrence dedup on the host
+    // (tables are small: at most one entry per frame)
+    std::vector<float4> cat((size_t)std::max<int64_t>(total_orient, 1));
+    {
+      int64_t o = 0;
+      for (int r = 0; r < n_parts; ++r) {
+        if (n_orient[r] > 0)
+          DARE_CUDA(cudaMemcpyAsync(cat.data() + o, d_orient[r], sizeof(float4) * n_orient[r],
+                                    cudaMemcpyDeviceToHost, s));
+        o += n_orient[r];
+      }
+      DARE_CUDA(cudaStreamSynchronize(s));
+    }
+    std::vector<uint32_t> word((size_t)std::max<int64_t>(total_orient, 1));
+    std::vector<uint8_t> zeros((size_t)std::max<int64_t>(total_orient, 1), 0);
+    std::vector<float4> table;
+    dedup_orientations(reinterpret_cast<const float*>(cat.data()), zeros.data(), total_orient, word.data(),
+                       table);
+    for (auto& w : word) w >>= 8;  // concatenated local id -> merged id
+
     auto vol = std::make_unique<dare_volume_s>();
     DARE_CUDA(cudaGetDevice(&vol->device));
     for (int a = 0; a < 3; ++a) {
@@ -90,30 +114,38 @@ extern "C" int dare_volume_merge(const double* origin, double voxel_size, const 
     vol->voxel = voxel_size;
     vol->ncells = ncells;
     vol->n_samples = total;
-    vol->n_orient = total_orient;
+    vol->n_orient = (int64_t)table.size();
     vol->rejected = total_rej;
 
+    Scratch<uint32_t> d_map((size_t)std::max<int64_t>(total_orient, 1), s);
+    DARE_CUDA(cudaMemcpyAsync(d_map.ptr, word.data(), sizeof(uint32_t) * word.size(), cudaMemcpyHostToDevice, s));
+    std::vector<const uint32_t*> remap(n_parts);
+    std::vector<const int8_t*> perms(n_parts);
+    {
+      int64_t o = 0;
+      for (int r = 0; r < n_parts; ++r) {
+        remap[r] = d_map.ptr + o;
+        perms[r] = d_perm ? d_perm[r] : nullptr;
+        o += n_orient[r];
+      }
+    }
     Scratch<const uint32_t*> d_off_ptrs(n_parts, s);
     Scratch<const uint4*> d_rec_ptrs(n_parts, s);
-    Scratch<uint32_t> d_base(n_parts, s);
-    DARE_CUDA(cudaMemcpyAsync(d_off_ptrs.ptr, d_offsets, sizeof(void*) * n_parts,
-                              cudaMemcpyHostToDevice, s));
-    DARE_CUDA(cudaMemcpyAsync(d_rec_ptrs.ptr, d_records, sizeof(void*) * n_parts,
-                              cudaMemcpyHostToDevice, s));
-    DARE_CUDA(cudaMemcpyAsync(d_base.ptr, orient_base.data(), sizeof(uint32_t) * n_parts,
-                              cudaMemcpyHostToDevice, s));
-    MergeParts parts{d_off_ptrs.ptr, d_rec_ptrs.ptr, d_base.ptr, n_parts};
+    Scratch<const int8_t*> d_perm_ptrs(n_parts, s);
+    Scratch<const uint32_t*> d_remap_ptrs(n_parts, s);
+    DARE_CUDA(cudaMemcpyAsync(d_off_ptrs.ptr, d_offsets, sizeof(void*) * n_parts, cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaMemcpyAsync(d_rec_ptrs.ptr, d_records, sizeof(void*) * n_parts, cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaMemcpyAsync(d_perm_ptrs.ptr, perms.data(), sizeof(void*) * n_parts, cudaMemcpyHostToDevice, s));
+    DARE_CUDA(cudaMemcpyAsync(d_remap_ptrs.ptr, remap.data(), sizeof(void*) * n_parts, cudaMemcpyHostToDevice,
+                              s));
+    MergeParts parts{d_off_ptrs.ptr, d_rec_ptrs.ptr, d_perm_ptrs.ptr, d_remap_ptrs.ptr, n_parts};
 
     dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
     dev_alloc(&vol->d_records, sizeof(uint4) * std::max<int64_t>(total, 1));
-    dev_alloc(&vol->d_orient, sizeof(float4) * std::max<int64_t>(total_orient, 1));
-    int64_t o = 0;
-    for (int r = 0; r < n_parts; ++r) {
-      if (n_orient[r] > 0)
-        DARE_CUDA(cudaMemcpyAsync(vol->d_orient + o, d_orient[r], sizeof(float4) * n_orient[r],
-                                  cudaMemcpyDeviceToDevice, s));
-      o += n_orient[r];
-    }
+    dev_alloc(&vol->d_orient, sizeof(float4) * std::max<size_t>(table.size(), 1));
+    if (!table.empty())
+      DARE_CUDA(cudaMemcpyAsync(vol->d_orient, table.data(), sizeof(float4) * table.size(),
+                                cudaMemcpyHostToDevice, s));
     Scratch<uint32_t> counts(ncells + 1, s);
     DARE_CUDA(cudaMemsetAsync(counts.ptr + ncells, 0, sizeof(uint32_t), s));
     merge_count_k<<<ceil_div(ncells, 256), 256, 0, s>>>(parts, ncells, counts.ptr);

@@ -1346,10 +1346,11 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
   DARE_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), s));
   // small calls from pageable memory (the latency path): stage through the
   // thread's pinned buffer -- async copies and a single synchronisation
-  const size_t out_bytes = npix + (packed ? nbits : npix);
-  const bool stage = out_bytes <= kStageMax && !host_pinned(pixels);
   const size_t pbytes = sizeof(double) * 14 * n_poses;
-  uint8_t* h_stage = stage ? (uint8_t*)thread_pinned(pbytes + fbo + sizeof(unsigned long long) + nbits) : nullptr;
+  // the whole staged block (params + outputs) is bounded, not just the outputs
+  const size_t stage_bytes = pbytes + fbo + sizeof(unsigned long long) + nbits;
+  const bool stage = stage_bytes <= kStageMax && !host_pinned(pixels);
+  uint8_t* h_stage = stage ? (uint8_t*)thread_pinned(stage_bytes) : nullptr;
   const double* h_params = params;
   if (stage) {
     memcpy(h_stage, params, pbytes);

@@ -101,10 +101,11 @@ void* thread_arena(int slot, size_t bytes, cudaStream_t s) {
   DARE_CUDA(cudaGetDevice(&dev));
   Block& b = arena.blocks[{dev, slot}];
   if (b.cap < bytes) {
+    const size_t old_cap = b.cap;
     if (b.p) DARE_CUDA(cudaFreeAsync(b.p, s));
     b.p = nullptr;
     b.cap = 0;
-    const size_t want = std::max(bytes, b.cap * 2);
+    const size_t want = std::max(bytes, old_cap * 2);  // geometric growth
     DARE_CUDA(cudaMallocAsync(&b.p, want, s));
     b.cap = want;
   }
@@ -125,8 +126,10 @@ void* thread_pinned(size_t bytes) {
     if (b.p) DARE_CUDA(cudaFreeHost(b.p));
     b.p = nullptr;
     b.cap = 0;
-    // geometric growth: pinned allocations are slow and cudaFreeHost synchronises
-    const size_t want = std::max<size_t>(std::max<size_t>(bytes, 8u << 20), 2 * old_cap);
+    // sized to the request (rounded to 64 KB) the first time -- a service's
+    // per-connection threads each own one -- then geometric growth: pinned
+    // allocations are slow and cudaFreeHost synchronises
+    const size_t want = std::max<size_t>((bytes + 0xffff) & ~(size_t)0xffff, 2 * old_cap);
     DARE_CUDA(cudaMallocHost(&b.p, want));
     b.cap = want;
   }
@@ -274,7 +277,9 @@ void FrameSet::wait_frames(cudaStream_t s, int64_t f_begin, int64_t f_end) const
 }
 
 FrameSet::~FrameSet() {
-  if (!done.empty()) cudaStreamWaitEvent(stream, done.back(), 0);  // copies finished before the free
+  // no DMA may still read the caller's host frames when the call returns (a
+  // block may reference only some upload groups): wait for the last copy
+  if (!done.empty()) cudaEventSynchronize(done.back());
   for (cudaEvent_t e : done) cudaEventDestroy(e);
   if (owned_frames) cudaFreeAsync(owned_frames, stream);
   if (d_image) cudaFreeAsync(d_image, stream);
@@ -289,6 +294,9 @@ dare_volume_s::~dare_volume_s() {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  // work enqueued by *_device calls on caller streams may still read the
+  // volume: nothing orders those streams before this free, so wait for the device
+  cudaDeviceSynchronize();
   dev_free(d_offsets);
   dev_free(d_records);
   dev_free(d_orient);

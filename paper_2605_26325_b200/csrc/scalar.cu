@@ -431,11 +431,11 @@ extern "C" int dare_scalar_upload(const double* origin, double voxel_size, const
     auto sv = new_scalar(origin, voxel_size, dims, counts != nullptr);
     cudaStream_t s = thread_stream();
     DARE_CUDA(cudaMemcpyAsync(sv->d_values, values, sizeof(float) * sv->ncells,
-                              cudaMemcpyHostToDevice, s));
-    DARE_CUDA(cudaMemcpyAsync(sv->d_flags, flags, sv->ncells, cudaMemcpyHostToDevice, s));
+                              cudaMemcpyDefault, s));
+    DARE_CUDA(cudaMemcpyAsync(sv->d_flags, flags, sv->ncells, cudaMemcpyDefault, s));
     if (counts)
       DARE_CUDA(cudaMemcpyAsync(sv->d_counts, counts, sizeof(int64_t) * sv->ncells,
-                                cudaMemcpyHostToDevice, s));
+                                cudaMemcpyDefault, s));
     DARE_CUDA(cudaStreamSynchronize(s));
     *out = sv.release();
   });

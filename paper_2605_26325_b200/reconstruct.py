@@ -38,6 +38,22 @@ def frames_arg(sweep, frames_device_ptr: int | None = None):
     return images, _lib.vptr(images), 0
 
 
+def frames_block(sweep, plan: FramePlan, start: int, end: int, frames_device_ptr: int | None = None):
+    """(n_images, pointer, on_device, frame_image, keepalive) for synchronized
+    frames [start, end): only the contiguous image range the block references
+    is passed (a frame-sharded rank uploads / reads its own images, not the
+    whole stack), frame_image rebased to it.  `keepalive` owns the memory the
+    pointer refers to (hold it until the call returns)."""
+    images, base_ptr, on_device = frames_arg(sweep, frames_device_ptr)
+    idx = np.ascontiguousarray(plan.image_index[start:end], dtype=np.int32)
+    if len(idx) == 0:
+        return 0, base_ptr, on_device, idx, images
+    i0, i1 = int(idx.min()), int(idx.max()) + 1
+    hw = int(plan.height) * int(plan.width)
+    ptr = ctypes.c_void_p((base_ptr.value or 0) + i0 * hw)
+    return i1 - i0, ptr, on_device, np.ascontiguousarray(idx - i0, dtype=np.int32), images
+
+
 def _mask(sweep):
     if sweep.mask is None:
         return None
@@ -48,8 +64,7 @@ def reconstruct_subset(sweep, plan: FramePlan, start: int, end: int, origin, vox
                        frames_device_ptr: int | None = None) -> DirectionalVolume:
     """Synchronized frames [start, end) into the given grid (the full grid for
     frame-sharded multi-GPU builds; start=0, end=n for a whole sweep)."""
-    images, frames_ptr, on_device = frames_arg(sweep, frames_device_ptr)
-    idx = np.ascontiguousarray(plan.image_index[start:end])
+    n_img, frames_ptr, on_device, idx, _keep = frames_block(sweep, plan, start, end, frames_device_ptr)
     axes = np.ascontiguousarray(plan.axes()[start:end])
     quats = np.ascontiguousarray(plan.canonical_quats_f32()[start:end])
     mask = _mask(sweep)
@@ -57,7 +72,7 @@ def reconstruct_subset(sweep, plan: FramePlan, start: int, end: int, origin, vox
     d = np.ascontiguousarray(dims, dtype=np.int64)
     raw = ctypes.c_void_p()
     rejected = ctypes.c_int64(0)
-    _lib.call("dare_reconstruct", frames_ptr, int(images.shape[0]), int(plan.height), int(plan.width),
+    _lib.call("dare_reconstruct", frames_ptr, n_img, int(plan.height), int(plan.width),
               on_device, _lib.ptr(idx, ctypes.c_int32), int(end - start),
               _lib.ptr(axes, ctypes.c_double), _lib.ptr(quats, ctypes.c_float),
               plan.pixel_pitch[0], plan.pixel_pitch[1], _lib.ptr(mask, ctypes.c_uint8),

@@ -21,6 +21,17 @@ def _sweep(seed, n=60, h=37, w=41):
     return db.SweepRecording(rng.integers(0, 256, (n, h, w), dtype=np.uint8), ts, ts, poses, (0.1, 0.1))
 
 
+def _raw(vol):
+    import torch
+
+    info = vol.device_info()
+    nc, n, no = int(np.prod(info.dims)), int(info.n_samples), int(info.n_orientations)
+    t = lambda p, shape, ts: torch.as_tensor(parallel._CudaArray(p, shape, ts), device="cuda").cpu().numpy()  # noqa
+    return {"offsets": t(info.d_cell_offsets, (nc + 1,), "<i4"), "records": t(info.d_records, (n, 4), "<i4"),
+            "perm": t(info.d_perm, (n,), "|i1"), "bins": t(info.d_bins, (nc,), "<i4"),
+            "orient": t(info.d_orientations, (no, 4), "<f4"), "n_orient": np.array(no)}
+
+
 @pytest.mark.parametrize("ranks", [1, 2, 3, 8])
 def test_merge_of_frame_blocks_equals_single_build(ranks):
     sweep = _sweep(ranks)
@@ -33,6 +44,14 @@ def test_merge_of_frame_blocks_equals_single_build(ranks):
     for name in ("cell_starts", "cell_counts", "positions", "orientations", "intensities"):
         np.testing.assert_array_equal(getattr(merged, name), getattr(full, name), err_msg=name)
     assert sum(p.rejected_out_of_bounds for p in parts) == full.rejected_out_of_bounds
+    # the device records themselves are identical in insertion order (read through
+    # perm), including the orientation ids: the merge deduplicates the parts'
+    # orientation tables, so merged replicas keep the single-orientation fast path
+    a, b = _raw(full), _raw(merged)
+    for name in ("offsets", "orient", "n_orient"):
+        np.testing.assert_array_equal(a[name], b[name], err_msg=name)
+    j = np.arange(len(a["perm"]))
+    np.testing.assert_array_equal(a["records"][j + a["perm"]], b["records"][j + b["perm"]])
 
 
 def test_merged_volume_reslices_identically():

@@ -1,11 +1,13 @@
 """Multi-process (world_size 2, gloo on CPU) tests of the sharded paths in
 paper_2605_26325_b200.parallel.  The collective logic (frame blocks, size
-exchange, padded all-gathers, rank-ordered merge, orientation-id rebasing,
-integer all-reduce) is the product code; only the per-rank compute is
+exchange, unpadded per-rank broadcasts, rank-ordered merge through perm,
+orientation-table dedup, integer all-reduce, scalar-grid broadcast and
+pose-sharded trilinear) is the product code; only the per-rank compute is
 replaced by the CPU oracle (OracleOps below), which mirrors the CUDA kernels.
 The result must equal the single-process oracle bit-for-bit."""
 import os
 import socket
+from types import SimpleNamespace
 
 import numpy as np
 import pytest
@@ -65,11 +67,25 @@ class OracleOps:
 
     @staticmethod
     def merge(parts, origin, voxel, dims):
+        """Rank-ordered run concatenation, records read through perm, orientation
+        tables deduplicated in rank order (first occurrence) -- merge.cu's rules."""
         nc = int(np.prod(dims))
         offs = [p.offsets.numpy().view(np.uint32).astype(np.int64) for p in parts]
-        recs = [p.records.numpy().view(np.uint32) for p in parts]
+        recs = []
+        for p in parts:
+            rec = p.records.numpy().view(np.uint32)
+            if p.perm is not None and len(rec):
+                j = np.arange(len(rec))
+                rec = rec[j + p.perm.numpy().astype(np.int64)]
+            recs.append(rec)
+        cat = np.concatenate([p.orient.numpy() for p in parts]) if sum(p.n_orient for p in parts) else \
+            np.zeros((0, 4), np.float32)
+        keys = [bytes(q.tobytes()) for q in cat]
+        first, remap_all = {}, []
+        for k in keys:
+            remap_all.append(first.setdefault(k, len(first)))
+        table = np.array([np.frombuffer(k, np.float32) for k in first]) if first else np.zeros((0, 4), np.float32)
         base = np.cumsum([0] + [p.n_orient for p in parts])
-        table = np.concatenate([p.orient.numpy() for p in parts]) if base[-1] else np.zeros((0, 4), np.float32)
         counts = sum(o[1:] - o[:-1] for o in offs)
         starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
         out = np.zeros((int(counts.sum()), 4), np.uint32)
@@ -77,12 +93,15 @@ class OracleOps:
             dst = starts[c]
             for r, (o, rec) in enumerate(zip(offs, recs)):
                 run = rec[o[c]:o[c + 1]].copy()
-                run[:, 3] = (((run[:, 3] >> 8) + base[r]) << 8) | (run[:, 3] & 0xFF)
+                local = run[:, 3] >> 8
+                run[:, 3] = (np.asarray(remap_all, np.uint32)[base[r] + local] << 8) | (run[:, 3] & 0xFF)
                 out[dst:dst + len(run)] = run
                 dst += len(run)
-        return oracle.OracleVolume(np.asarray(origin, float), voxel, tuple(dims), starts, counts,
-                                   out[:, :3].copy().view(np.float32), table[out[:, 3] >> 8],
-                                   (out[:, 3] & 0xFF).astype(np.uint8))
+        vol = oracle.OracleVolume(np.asarray(origin, float), voxel, tuple(dims), starts, counts,
+                                  out[:, :3].copy().view(np.float32), table[out[:, 3] >> 8],
+                                  (out[:, 3] & 0xFF).astype(np.uint8))
+        vol.n_orient = len(table)
+        return vol
 
     @staticmethod
     def reslice_block(volume, planes, cfg):
@@ -114,7 +133,24 @@ class OracleOps:
         values, flags = np.empty(nc, np.float32), np.empty(nc, np.uint8)
         oracle.load().oracle_compound_finalize(nc, sums.ctypes.data, counts.ctypes.data, values.ctypes.data,
                                                flags.ctypes.data)
-        return values, flags, counts
+        return SimpleNamespace(origin=tuple(float(x) for x in origin), voxel_size=float(voxel), dims=tuple(dims),
+                               values=values, flags=flags, counts=counts)
+
+    @staticmethod
+    def scalar_tensors(volume):
+        return torch.from_numpy(np.ascontiguousarray(volume.values)), torch.from_numpy(
+            np.ascontiguousarray(volume.flags))
+
+    @staticmethod
+    def scalar_from_tensors(origin, voxel, dims, values, flags):
+        return SimpleNamespace(origin=origin, voxel_size=voxel, dims=dims, values=values.numpy(),
+                               flags=flags.numpy(), counts=None)
+
+    @staticmethod
+    def trilinear_block(volume, planes):
+        res = [oracle.trilinear(volume.origin, volume.voxel_size, volume.dims, volume.values, volume.flags,
+                                oracle.plane_params(p), p.width, p.height) for p in planes]
+        return np.stack([r[0] for r in res]), np.stack([r[1] for r in res])
 
 
 def _worker(rank, world, port, q):
@@ -135,11 +171,22 @@ def _worker(rank, world, port, q):
             rp, rc = oracle.reslice(full, oracle.plane_params(p), oracle.cfg_array(cfg), p.width, p.height)
             np.testing.assert_array_equal(px[k], rp)
             np.testing.assert_array_equal(cov[k], rc)
-        values, flags, counts = parallel.compound_sharded(sweep, 0.125, 0.0, ops=OracleOps)
-        _, _, _, rv, rf, rc = oracle.compound(sweep, 0.125, 0.0)
-        np.testing.assert_array_equal(values, rv)
-        np.testing.assert_array_equal(flags, rf)
-        np.testing.assert_array_equal(counts, rc)
+        sv = parallel.compound_sharded(sweep, 0.125, 0.0, ops=OracleOps)
+        o, vx, dims, rv, rf, rc = oracle.compound(sweep, 0.125, 0.0)
+        np.testing.assert_array_equal(sv.values, rv)
+        np.testing.assert_array_equal(sv.flags, rf)
+        np.testing.assert_array_equal(sv.counts, rc)
+        # pose-sharded trilinear: rank 0's filled grid is broadcast, each rank
+        # reslices its pose block, results gathered in pose order
+        fv, ff = oracle.fill_holes(rv, rf, dims, 3)
+        grid = SimpleNamespace(origin=o, voxel_size=vx, dims=tuple(dims), values=fv, flags=ff) if rank == 0 \
+            else None
+        tpx, tcov, _ = parallel.reslice_trilinear_sharded(grid, planes, ops=OracleOps)
+        for k, p in enumerate(planes):
+            rp, rc2, _ = oracle.trilinear(o, vx, dims, fv, ff, oracle.plane_params(p), p.width, p.height)
+            np.testing.assert_array_equal(tpx[k], rp)
+            np.testing.assert_array_equal(tcov[k], rc2)
+        assert tcov.any()
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # report to the parent
