@@ -296,6 +296,14 @@ int dare_reslice_trilinear_device(dare_scalar_t vol, int32_t n_poses, const doub
 /* ---- diagnostics -------------------------------------------------------- */
 /* Device restatement of glibc exp on n device doubles (parity tests). */
 int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream);
+/* Host-only diagnostic: the exact per-axis threshold tables the count and
+ * compound passes use for a grid (T[k] = smallest f64 world coordinate whose
+ * reference cell index floor((f64(f32(P)) - o) / v) is >= k; with zfine the z
+ * table interleaves the z-quarter bin bounds).  out holds (nx+1) + (ny+1) +
+ * (nz+1, or 4 nz + 1 with zfine) doubles; n_out[3] = intervals per table
+ * (-1 when the fine table is not monotone). */
+int dare_cell_thresholds(const double* origin, double voxel_size, const int64_t* dims, int32_t zfine,
+                         double* out, int64_t* n_out);
 /* Pixels the last dare_reslice / dare_reslice_bruteforce call on this thread
  * recomputed on the exact FP64 path because the certified bound was
  * inconclusive (0 with cfg.exact = 1, or when the fast path is disabled). */

@@ -116,6 +116,7 @@ _SIGNATURES = {
     "dare_exp_device": [c_vp, c_vp, c_i64, c_vp],
     "dare_reslice_last_fallback": [P_i64],
     "dare_fastmath_check": [P_f64, P_f64, P_i32],
+    "dare_cell_thresholds": [P_f64, c_f64, P_i64, c_i32, P_f64, P_i64],
 }
 
 EXPORTED = ["dare_last_error", *_SIGNATURES]

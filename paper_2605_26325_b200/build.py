@@ -19,8 +19,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdare_b200.so")
 SOURCES = ["runtime.cu", "reconstruct.cu", "volume_api.cu", "reslice.cu", "scalar.cu", "merge.cu", "bins.cu",
-           "plan.cu"]
-HEADERS = ["common.cuh", "volume.cuh", "dare_exp.h", "exp_table.h"]
+           "plan.cu", "cells.cu"]
+HEADERS = ["common.cuh", "volume.cuh", "cells.cuh", "dare_exp.h", "exp_table.h"]
 
 
 def nvcc_path() -> str:

@@ -30,6 +30,7 @@
 #include <memory>
 #include <vector>
 
+#include "cells.cuh"
 #include "volume.cuh"
 
 namespace dare {
@@ -214,6 +215,101 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
       }
     }
     if (lin >= 0) bb |= (uint32_t)((z >= zb1) + (z >= zb2) + (z >= zb3)) << (2 * k);
+    ++k;
+  }
+  if (cur >= 0) {
+    atomicAdd(&counts[cur], k);
+    my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
+    ++nr;
+  }
+  nruns[blk * 256 + threadIdx.x] = (uint8_t)nr;  // <= kRunFrames
+  const unsigned oob = __reduce_add_sync(0xffffffffu, n_oob);  // one atomic per warp
+  if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);
+}
+
+// Count pass on the exact threshold tables (cells.cuh): per frame the pixel's
+// world point P (the reference's FP64 chain, reconstruct.py:156-162) is
+// compared with the [lo, hi) interval of its current cell per axis (z on the
+// fine cell/quarter table, so the z bin comes with it); only a crossing walks
+// the tables.  No f32 rounding, division or float->int conversion per frame.
+// Consecutive frames with bit-identical axis columns R[:,0], R[:,1] (sweeps
+// at a fixed probe orientation) reuse U*R[a,0] + V*R[a,1]: the same f64 value
+// the reference computes, so P = that + t[a] is bit-identical.  Output (run
+// records, histogram, out-of-bounds tally) is exactly frame_count_k's.
+__global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTables ct, VoxelMap m,
+                                                           uint32_t* counts, uint2* __restrict__ runs,
+                                                           uint8_t* __restrict__ nruns,
+                                                           unsigned long long* rejected) {
+  __shared__ double s_axes[kRunFrames * 9];
+  __shared__ int s_same[kRunFrames];
+  uint32_t u, v;
+  tile_pixel(fv, u, v);
+  const uint32_t lane = lane_id();
+  const uint32_t p = v * fv.W + u;
+  const bool in_frame = u < fv.W && v < fv.H && (!fv.mask || fv.mask[p] != 0);
+  const uint32_t f0 = blockIdx.y * kRunFrames;
+  const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[(size_t)f0 * 9 + i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < nf; j += blockDim.x) {
+    bool same = j > 0;
+    for (int c = 0; c < 6 && same; ++c)
+      same = __double_as_longlong(s_axes[j * 9 + c]) == __double_as_longlong(s_axes[(j - 1) * 9 + c]);
+    s_same[j] = same;
+  }
+  __syncthreads();
+  const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+  uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
+  const double U = (double)u * fv.px, V = (double)v * fv.py;
+  const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
+  AxisCell ax[3];
+  double S[3];
+  for (int a = 0; a < 3; ++a) {
+    ax[a].g = -2;  // unknown: the first frame locates from a guess
+    ax[a].lo = ax[a].hi = 0.0;
+    S[a] = 0.0;
+  }
+  int32_t cur = -1;
+  uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_oob = 0;
+  for (int j = 0; j < nf; ++j) {  // block-uniform trip count and branches
+    const double* fa = s_axes + j * 9;
+    double P[3];
+    if (s_same[j]) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) P[a] = S[a] + fa[6 + a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        S[a] = U * fa[a] + V * fa[3 + a];
+        P[a] = S[a] + fa[6 + a];
+      }
+    }
+    if (!(axis_same(P[0], ax[0]) && axis_same(P[1], ax[1]) && axis_same(P[2], ax[2]))) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (ax[a].g == -2) ax[a].g = axis_guess(P[a], m.origin[a], m.inv_voxel, ct.n[a], a == 2);
+        axis_locate(P[a], ct.t[a], ct.n[a], ax[a]);
+      }
+    }
+    const int gz = ax[2].g;
+    const bool ok = ax[0].g >= 0 && ax[0].g < ct.n[0] && ax[1].g >= 0 && ax[1].g < ct.n[1] && gz >= 0 &&
+                    gz < ct.n[2];
+    const int32_t cell = ok ? (int32_t)(((uint32_t)ax[0].g * ny + (uint32_t)ax[1].g) * nz + ((uint32_t)gz >> 2)) : -1;
+    const int32_t lin = in_frame ? cell : -1;
+    n_oob += (in_frame && cell < 0) ? 1u : 0u;
+    const bool restart = lin != cur || k == (uint32_t)kMaxRun;
+    if (restart && cur >= 0) {
+      atomicAdd(&counts[cur], k);
+      my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
+      ++nr;
+    }
+    if (restart) {
+      cur = lin;
+      run_j = (uint32_t)j;
+      k = 0;
+      bb = 0;
+    }
+    if (lin >= 0) bb |= ((uint32_t)gz & 3u) << (2 * k);
     ++k;
   }
   if (cur >= 0) {
@@ -763,12 +859,21 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     // per-thread run lists of the count pass (8 B per run, <= one run per frame)
     Scratch<uint2> runs(n_frames > 0 ? (size_t)tiles * chunks * kRunFrames * 256 : 0, s);
     Scratch<uint8_t> nruns(n_frames > 0 ? (size_t)tiles * chunks * 256 : 0, s);
+    // exact per-axis threshold tables (cells.cuh); the plain kernel when the
+    // fine z table is not monotone or the development switch asks for it
+    Scratch<double> tab_store;
+    CellTables ct;
+    const char* legacy = getenv("DARE_COUNT_LEGACY");
+    const bool tabs_ok = !(legacy && legacy[0] == '1') && build_cell_tables(m, true, s, tab_store, ct);
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
                        unsigned long long* keys, unsigned long long* rej) {
       if (n_frames == 0) return;
       if (!fill) {  // needs no intensities: runs while host frames are still uploading
-        (m.exact_inv ? frame_count_k<true> : frame_count_k<false>)<<<dim3(tiles, chunks), 256, 0, s>>>(
-            fv, m, counts, runs.ptr, nruns.ptr, rej);
+        if (tabs_ok)
+          frame_count_tab_k<<<dim3(tiles, chunks), 256, 0, s>>>(fv, ct, m, counts, runs.ptr, nruns.ptr, rej);
+        else
+          (m.exact_inv ? frame_count_k<true> : frame_count_k<false>)<<<dim3(tiles, chunks), 256, 0, s>>>(
+              fv, m, counts, runs.ptr, nruns.ptr, rej);
         return;
       }
       // fill in groups of chunks, each launched once its images are resident

@@ -20,6 +20,7 @@
 #include <memory>
 #include <vector>
 
+#include "cells.cuh"
 #include "volume.cuh"
 
 namespace dare {
@@ -97,6 +98,97 @@ __global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m
     cnt += 1;
   }
   if (__any_sync(0xffffffffu, cur >= 0)) compound_flush(cur >= 0, cur, sum, cnt, sums, counts);
+}
+
+// compound_k on the exact threshold tables (cells.cuh; same integer sums):
+// per frame two compares per axis against the current cell's interval, the
+// f64 in-plane product reused across frames with identical axis columns,
+// 32-bit cells and a 32-bit MATCH for the warp-aggregated flush.
+__device__ __forceinline__ void compound_flush32(bool need, int32_t lin, unsigned sum, unsigned cnt,
+                                                 unsigned long long* sums, unsigned long long* counts) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned key = need ? (unsigned)lin : (0x80000000u | lane);
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const unsigned total = __reduce_add_sync(peers, sum);
+  const unsigned n = __reduce_add_sync(peers, cnt);
+  if (need && lane == (unsigned)(__ffs(peers) - 1)) {
+    atomicAdd(&sums[lin], (unsigned long long)total);
+    atomicAdd(&counts[lin], (unsigned long long)n);
+  }
+}
+
+__global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTables ct, VoxelMap m,
+                                                      unsigned long long* sums, unsigned long long* counts) {
+  __shared__ double s_axes[kCFrames * 9];
+  __shared__ long long s_img[kCFrames];
+  __shared__ int s_same[kCFrames];
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t W = (uint32_t)fv.W, H = (uint32_t)fv.H;
+  const uint32_t tiles_u = (W + 15) / 16;
+  const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
+  const uint32_t p = v * W + u;
+  const bool in_frame = u < W && v < H && (!fv.mask || fv.mask[p] != 0);
+  const long long hw = (long long)H * W;
+  const int64_t f0 = (int64_t)blockIdx.y * kCFrames;
+  const int nf = (int)min((int64_t)kCFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[f0 * 9 + i];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (long long)fv.image[f0 + i] * hw;
+  __syncthreads();
+  for (int j = threadIdx.x; j < nf; j += blockDim.x) {
+    bool same = j > 0;
+    for (int c = 0; c < 6 && same; ++c)
+      same = __double_as_longlong(s_axes[j * 9 + c]) == __double_as_longlong(s_axes[(j - 1) * 9 + c]);
+    s_same[j] = same;
+  }
+  __syncthreads();
+  const double U = (double)u * fv.px, V = (double)v * fv.py;
+  const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
+  AxisCell ax[3];
+  double S[3];
+  for (int a = 0; a < 3; ++a) {
+    ax[a].g = -2;
+    ax[a].lo = ax[a].hi = 0.0;
+    S[a] = 0.0;
+  }
+  int32_t cur = -1;
+  unsigned sum = 0, cnt = 0;
+  for (int j = 0; j < nf; ++j) {  // block-uniform trip count
+    const double* fa = s_axes + j * 9;
+    double P[3];
+    if (s_same[j]) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) P[a] = S[a] + fa[6 + a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        S[a] = U * fa[a] + V * fa[3 + a];
+        P[a] = S[a] + fa[6 + a];
+      }
+    }
+    if (!(axis_same(P[0], ax[0]) && axis_same(P[1], ax[1]) && axis_same(P[2], ax[2]))) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (ax[a].g == -2) ax[a].g = axis_guess(P[a], m.origin[a], m.inv_voxel, ct.n[a], 0);
+        axis_locate(P[a], ct.t[a], ct.n[a], ax[a]);
+      }
+    }
+    const bool ok = in_frame && ax[0].g >= 0 && ax[0].g < ct.n[0] && ax[1].g >= 0 && ax[1].g < ct.n[1] &&
+                    ax[2].g >= 0 && ax[2].g < ct.n[2];
+    const int32_t lin = ok ? (int32_t)(((uint32_t)ax[0].g * ny + (uint32_t)ax[1].g) * nz + (uint32_t)ax[2].g) : -1;
+    const unsigned inten = in_frame ? (unsigned)fv.frames[s_img[j] + p] : 0u;
+    const bool change = lin != cur;
+    const bool need = change && cur >= 0;
+    if (__any_sync(0xffffffffu, need)) compound_flush32(need, cur, sum, cnt, sums, counts);
+    if (change) {
+      cur = lin;
+      sum = 0;
+      cnt = 0;
+    }
+    sum += inten;
+    cnt += 1;
+  }
+  if (__any_sync(0xffffffffu, cur >= 0)) compound_flush32(cur >= 0, cur, sum, cnt, sums, counts);
 }
 
 __global__ void compound_finalize_k(int64_t n, const unsigned long long* __restrict__ sums,
@@ -366,8 +458,15 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
       PhaseTimer pt(s, "compound_accumulate");
       DARE_LIMIT(ceil_div(n_frames, kCFrames) <= 65535, "too many frames for one compound launch");
       dim3 grid(ceil_div(width, 16) * ceil_div(height, 16), ceil_div(n_frames, kCFrames));
-      (m.exact_inv ? compound_k<true> : compound_k<false>)<<<grid, 256, 0, s>>>(
-          fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
+      Scratch<double> tab_store;
+      CellTables ct;
+      const char* legacy = getenv("DARE_COUNT_LEGACY");
+      if (!(legacy && legacy[0] == '1') && m.dims[0] * m.dims[1] * m.dims[2] < (int64_t)INT32_MAX &&
+          build_cell_tables(m, false, s, tab_store, ct))
+        compound_tab_k<<<grid, 256, 0, s>>>(fv, ct, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
+      else
+        (m.exact_inv ? compound_k<true> : compound_k<false>)<<<grid, 256, 0, s>>>(
+            fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
       pt.mark("compound_k");
       DARE_CUDA(cudaGetLastError());
     }
