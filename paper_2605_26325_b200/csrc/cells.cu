@@ -1,6 +1,7 @@
 // Host construction of the exact per-axis threshold tables (cells.cuh).
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 #include "cells.cuh"
 #include "volume.cuh"
@@ -31,18 +32,22 @@ double ref_quotient(double P, const VoxelMap& m, int a) {
 }
 
 // Smallest double P with pred(P) true (pred monotone false -> true over the
-// non-NaN doubles); +inf when it never holds below +inf.  A narrow bracket
-// around `guess` is tried first; the full range otherwise.
+// non-NaN doubles); +inf when it never holds below +inf.  The search brackets
+// the answer by doubling a window around `guess` (the true threshold is a few
+// ulps from it), then bisects; the full range is the fallback.
 template <class Pred>
 double threshold(Pred pred, double guess) {
   const uint64_t lo_all = okey(-HUGE_VAL), hi_all = okey(HUGE_VAL);
   uint64_t lo = lo_all, hi = hi_all;  // invariant: pred(lo) false, pred(hi) true
   if (std::isfinite(guess)) {
-    const uint64_t g = okey(guess), w = 1ull << 24;
-    const uint64_t a = g > lo_all + w ? g - w : lo_all, b = g < hi_all - w ? g + w : hi_all;
-    if (!pred(from_okey(a)) && pred(from_okey(b))) {
-      lo = a;
-      hi = b;
+    const uint64_t g = okey(guess);
+    for (uint64_t w = 4; w <= (1ull << 40); w <<= 3) {
+      const uint64_t a = g > lo_all + w ? g - w : lo_all, b = g < hi_all - w ? g + w : hi_all;
+      if (!pred(from_okey(a)) && pred(from_okey(b))) {
+        lo = a;
+        hi = b;
+        break;
+      }
     }
   }
   if (pred(from_okey(lo))) return from_okey(lo);
@@ -57,6 +62,22 @@ double threshold(Pred pred, double guess) {
   return from_okey(hi);
 }
 
+// Smallest double P with (float)P >= ps (ps finite): just above or at the
+// midpoint between ps and its f32 predecessor (ties round to the even one).
+double float_threshold(float ps) {
+  const float pm = std::nextafter(ps, -HUGE_VALF);
+  const double mid = 0.5 * ((double)pm + (double)ps);  // exact
+  return (float)mid >= ps ? mid : std::nextafter(mid, HUGE_VAL);
+}
+
+// T with pred(T) true and pred(prev(T)) false when `cand` is right, else the
+// bisection.  pred over doubles is what defines the table.
+template <class Pred>
+double checked(Pred pred, double cand, double guess) {
+  if (std::isfinite(cand) && pred(cand) && !pred(std::nextafter(cand, -HUGE_VAL))) return cand;
+  return threshold(pred, guess);
+}
+
 }  // namespace
 
 bool build_cell_tables_host(const VoxelMap& m, bool zfine, std::vector<double>& host, size_t off[3],
@@ -66,9 +87,17 @@ bool build_cell_tables_host(const VoxelMap& m, bool zfine, std::vector<double>& 
     const int64_t n = m.dims[a];
     off[a] = host.size();
     std::vector<double> T((size_t)n + 1);
-    for (int64_t k = 0; k <= n; ++k)
-      T[k] = threshold([&](double P) { return ref_quotient(P, m, a) >= (double)k; },
-                       m.origin[a] + (double)k * m.voxel);
+    for (int64_t k = 0; k <= n; ++k) {
+      auto pred = [&](double P) { return ref_quotient(P, m, a) >= (double)k; };
+      // the smallest f32 p with quotient >= k, by f32 steps from the nearest guess,
+      // then the smallest f64 rounding to it
+      const double guess = m.origin[a] + (double)k * m.voxel;
+      float p = (float)guess;
+      for (int i = 0; i < 16 && ref_quotient((double)std::nextafter(p, -HUGE_VALF), m, a) >= (double)k; ++i)
+        p = std::nextafter(p, -HUGE_VALF);
+      for (int i = 0; i < 16 && !(ref_quotient((double)p, m, a) >= (double)k); ++i) p = std::nextafter(p, HUGE_VALF);
+      T[k] = checked(pred, float_threshold(p), guess);
+    }
     if (a == 2 && zfine) {
       // fine table: cell boundaries interleaved with the z-quarter bounds
       // zb(iz, b) = f32(oz + (iz + b/4) v) (volume.cuh zbin_bound, same expression)
@@ -77,7 +106,7 @@ bool build_cell_tables_host(const VoxelMap& m, bool zfine, std::vector<double>& 
         F[4 * iz] = T[iz];
         for (int b = 1; b <= 3; ++b) {
           const float zb = (float)(m.origin[2] + ((double)iz + 0.25 * b) * m.voxel);
-          F[4 * iz + b] = threshold([&](double P) { return (float)P >= zb; }, (double)zb);
+          F[4 * iz + b] = checked([&](double P) { return (float)P >= zb; }, float_threshold(zb), (double)zb);
         }
       }
       F[4 * n] = T[n];
@@ -95,9 +124,46 @@ bool build_cell_tables_host(const VoxelMap& m, bool zfine, std::vector<double>& 
 
 bool build_cell_tables(const VoxelMap& m, bool zfine, cudaStream_t s, Scratch<double>& storage,
                        CellTables& out) {
+  // small per-process cache: rebuilding a volume on the same grid reuses the tables
+  struct Entry {
+    double key[8];
+    std::vector<double> host;
+    size_t off[3];
+    int n[3];
+    bool ok;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;  // most recent last, <= 8 entries
+  const double key[8] = {m.origin[0], m.origin[1], m.origin[2], m.voxel, (double)m.dims[0], (double)m.dims[1],
+                         (double)m.dims[2], zfine ? 1.0 : 0.0};
   std::vector<double> host;
   size_t off[3];
-  if (!build_cell_tables_host(m, zfine, host, off, out.n)) return false;
+  bool ok = false, hit = false;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+      if (std::memcmp(e.key, key, sizeof(key)) == 0) {
+        host = e.host;
+        std::memcpy(off, e.off, sizeof(off));
+        std::memcpy(out.n, e.n, sizeof(e.n));
+        ok = e.ok;
+        hit = true;
+        break;
+      }
+  }
+  if (!hit) {
+    ok = build_cell_tables_host(m, zfine, host, off, out.n);
+    std::lock_guard<std::mutex> lock(mu);
+    Entry e;
+    std::memcpy(e.key, key, sizeof(key));
+    e.host = host;
+    std::memcpy(e.off, off, sizeof(off));
+    std::memcpy(e.n, out.n, sizeof(e.n));
+    e.ok = ok;
+    if (cache.size() >= 8) cache.erase(cache.begin());
+    cache.push_back(std::move(e));
+  }
+  if (!ok) return false;
   out.zfine = zfine ? 1 : 0;
   // storage is an empty Scratch owned by the caller (freed on its scope exit)
   DARE_CUDA(cudaMallocAsync((void**)&storage.ptr, sizeof(double) * host.size(), s));

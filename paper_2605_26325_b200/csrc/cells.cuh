@@ -67,6 +67,40 @@ __device__ __forceinline__ void axis_locate(double P, const double* __restrict__
 
 __device__ __forceinline__ bool axis_same(double P, const AxisCell& a) { return a.lo <= P && P < a.hi; }
 
+// z on the fine table, tracked at cell granularity: the interval is the cell
+// [F[4g], F[4g+4]) and q1..q3 = F[4g+1..3] give the quarter bin by compares.
+struct AxisCellZ {
+  int g;  // cell index, -1 below, n at/above (out of bounds)
+  double lo, hi, q1, q2, q3;
+  __device__ __forceinline__ uint32_t bin(double P) const {
+    return (uint32_t)(P >= q1) + (uint32_t)(P >= q2) + (uint32_t)(P >= q3);
+  }
+};
+
+__device__ __forceinline__ void axis_locate_z(double P, const double* __restrict__ F, int n, AxisCellZ& a) {
+  if (!(P == P)) {
+    a.g = -1;
+    a.lo = a.hi = P;
+    return;
+  }
+  int g = a.g;
+  if (g < -1 || g > n) g = -1;
+  while (g < n && __ldg(F + 4 * (g + 1)) <= P) ++g;
+  while (g >= 0 && P < __ldg(F + 4 * g)) --g;
+  a.g = g;
+  if (g >= 0 && g < n) {
+    a.lo = __ldg(F + 4 * g);
+    a.q1 = __ldg(F + 4 * g + 1);
+    a.q2 = __ldg(F + 4 * g + 2);
+    a.q3 = __ldg(F + 4 * g + 3);
+    a.hi = __ldg(F + 4 * g + 4);
+  } else {
+    a.lo = g < 0 ? -CUDART_INF : __ldg(F + 4 * n);
+    a.hi = g < 0 ? __ldg(F) : CUDART_INF;
+    a.q1 = a.q2 = a.q3 = CUDART_INF;
+  }
+}
+
 // First guess of the interval of P (any value works; it only shortens the walk).
 __device__ __forceinline__ int axis_guess(double P, double origin, double inv_voxel, int n, int fine) {
   const double q = (P - origin) * inv_voxel * (fine ? 4.0 : 1.0);

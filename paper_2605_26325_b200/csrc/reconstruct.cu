@@ -262,15 +262,21 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
-  AxisCell ax[3];
+  AxisCell ax[2];
+  AxisCellZ az;
   double S[3];
-  for (int a = 0; a < 3; ++a) {
+  for (int a = 0; a < 2; ++a) {
     ax[a].g = -2;  // unknown: the first frame locates from a guess
     ax[a].lo = ax[a].hi = 0.0;
-    S[a] = 0.0;
   }
+  az.g = -2;
+  az.lo = az.hi = az.q1 = az.q2 = az.q3 = 0.0;
+  for (int a = 0; a < 3; ++a) S[a] = 0.0;
+  const int nzc = ct.n[2] >> 2;  // cells along z (the fine table has 4 per cell)
+  // the current frame's cell (-1 out of bounds), recomputed only on a crossing
+  int32_t tracked = -1;
   int32_t cur = -1;
-  uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_oob = 0;
+  uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_in = 0;
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count and branches
     const double* fa = s_axes + j * 9;
     double P[3];
@@ -284,24 +290,32 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
         P[a] = S[a] + fa[6 + a];
       }
     }
-    if (!(axis_same(P[0], ax[0]) && axis_same(P[1], ax[1]) && axis_same(P[2], ax[2]))) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (ax[a].g == -2) ax[a].g = axis_guess(P[a], m.origin[a], m.inv_voxel, ct.n[a], a == 2);
-        axis_locate(P[a], ct.t[a], ct.n[a], ax[a]);
+    const bool sx = axis_same(P[0], ax[0]), sy = axis_same(P[1], ax[1]);
+    const bool sz = az.lo <= P[2] && P[2] < az.hi;
+    if (!(sx & sy & sz)) {  // a crossing: relocate only the axes the point left
+      if (!sx) {
+        if (ax[0].g == -2) ax[0].g = axis_guess(P[0], m.origin[0], m.inv_voxel, ct.n[0], 0);
+        axis_locate(P[0], ct.t[0], ct.n[0], ax[0]);
       }
+      if (!sy) {
+        if (ax[1].g == -2) ax[1].g = axis_guess(P[1], m.origin[1], m.inv_voxel, ct.n[1], 0);
+        axis_locate(P[1], ct.t[1], ct.n[1], ax[1]);
+      }
+      if (!sz) {
+        if (az.g == -2) az.g = axis_guess(P[2], m.origin[2], m.inv_voxel, nzc, 0);
+        axis_locate_z(P[2], ct.t[2], nzc, az);
+      }
+      const bool ok = (unsigned)ax[0].g < (unsigned)ct.n[0] && (unsigned)ax[1].g < (unsigned)ct.n[1] &&
+                      (unsigned)az.g < (unsigned)nzc;
+      tracked = ok ? (int32_t)(((uint32_t)ax[0].g * ny + (uint32_t)ax[1].g) * nz + (uint32_t)az.g) : -1;
     }
-    const int gz = ax[2].g;
-    const bool ok = ax[0].g >= 0 && ax[0].g < ct.n[0] && ax[1].g >= 0 && ax[1].g < ct.n[1] && gz >= 0 &&
-                    gz < ct.n[2];
-    const int32_t cell = ok ? (int32_t)(((uint32_t)ax[0].g * ny + (uint32_t)ax[1].g) * nz + ((uint32_t)gz >> 2)) : -1;
-    const int32_t lin = in_frame ? cell : -1;
-    n_oob += (in_frame && cell < 0) ? 1u : 0u;
+    const int32_t lin = in_frame ? tracked : -1;
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     if (restart && cur >= 0) {
       atomicAdd(&counts[cur], k);
       my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
       ++nr;
+      n_in += k;
     }
     if (restart) {
       cur = lin;
@@ -309,14 +323,17 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
       k = 0;
       bb = 0;
     }
-    if (lin >= 0) bb |= ((uint32_t)gz & 3u) << (2 * k);
+    bb |= az.bin(P[2]) << (2 * k);  // (garbage for out-of-bounds runs: never stored)
     ++k;
   }
   if (cur >= 0) {
     atomicAdd(&counts[cur], k);
     my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
     ++nr;
+    n_in += k;
   }
+  // out-of-bounds samples = the frames of in-frame pixels not in a kept run
+  const uint32_t n_oob = in_frame ? (uint32_t)nf - n_in : 0u;
   nruns[blk * 256 + threadIdx.x] = (uint8_t)nr;  // <= kRunFrames
   const unsigned oob = __reduce_add_sync(0xffffffffu, n_oob);  // one atomic per warp
   if (lane == 0 && oob) atomicAdd(rejected, (unsigned long long)oob);

@@ -166,9 +166,9 @@ __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTa
         P[a] = S[a] + fa[6 + a];
       }
     }
-    if (!(axis_same(P[0], ax[0]) && axis_same(P[1], ax[1]) && axis_same(P[2], ax[2]))) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
+    for (int a = 0; a < 3; ++a) {  // relocate only the axes whose interval the point left
+      if (!axis_same(P[a], ax[a])) {
         if (ax[a].g == -2) ax[a].g = axis_guess(P[a], m.origin[a], m.inv_voxel, ct.n[a], 0);
         axis_locate(P[a], ct.t[a], ct.n[a], ax[a]);
       }
