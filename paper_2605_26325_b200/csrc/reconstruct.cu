@@ -140,6 +140,7 @@ constexpr int kMaxRun = 8;  // bins of a run's samples fit 16 bits
 // insertion order.
 constexpr int kKeyShift = 10;
 
+
 template <bool kInv>
 __device__ __forceinline__ int32_t frame_cell32(const double* fa, double U, double V, const VoxelMap& m,
                                                 float& z32, uint32_t& iz) {
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
 // at a fixed probe orientation) reuse U*R[a,0] + V*R[a,1]: the same f64 value
 // the reference computes, so P = that + t[a] is bit-identical.  Output (run
 // records, histogram, out-of-bounds tally) is exactly frame_count_k's.
+template <bool kBins>
 __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTables ct, VoxelMap m,
                                                            uint32_t* counts, uint2* __restrict__ runs,
                                                            uint8_t* __restrict__ nruns,
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
       k = 0;
       bb = 0;
     }
-    bb |= az.bin(P[2]) << (2 * k);  // (garbage for out-of-bounds runs: never stored)
+    if constexpr (kBins) bb |= az.bin(P[2]) << (2 * k);  // (garbage for out-of-bounds runs: never stored)
     ++k;
   }
   if (cur >= 0) {
@@ -341,11 +343,17 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
 
 // Fill pass over the chunks [chunk_begin, chunk_begin + gridDim.y): replays
 // each thread's runs (see frame_count_k); no pixel geometry is recomputed.
+// Key = u64: insertion index << kKeyShift | z bin << 8 | intensity.  Key = u32
+// (when the packed (frame, v, u) index and the 2-bit z bin fit 32 bits):
+// insertion index << 2 | z bin -- half the key traffic; the seal then reads
+// the intensity from the frame.
+template <class Key>
 __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk_begin,
                                                     const uint2* __restrict__ runs,
                                                     const uint8_t* __restrict__ nruns, uint32_t* counts,
                                                     const uint32_t* __restrict__ offsets,
-                                                    unsigned long long* keys) {
+                                                    Key* keys) {
+  constexpr bool kWide = sizeof(Key) == 8;
   __shared__ uint32_t s_img[kRunFrames];
   uint32_t u, v;
   tile_pixel(fv, u, v);
@@ -369,7 +377,7 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     uint32_t inten[kMaxRun];
 #pragma unroll
     for (int t = 0; t < kMaxRun; ++t)
-      inten[t] = (need && (uint32_t)t < k) ? fv.frames[(size_t)s_img[run_j + t] * fv.hw + p] : 0u;
+      inten[t] = (kWide && need && (uint32_t)t < k) ? fv.frames[(size_t)s_img[run_j + t] * fv.hw + p] : 0u;
     const uint32_t cell_off = need ? offsets[lin] : 0u;  // issued early: overlaps the atomic
     // lanes not emitting get a key no cell has, so MATCH runs on the full warp
     const unsigned peers = __match_any_sync(0xffffffffu, need ? lin : (0x80000000u | lane));
@@ -397,14 +405,25 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
       const uint32_t stride = uniform ? n : 1u;
-      unsigned long long* dst = keys + cell_off + base + (uniform ? rank : prefix);
-      const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
-      const unsigned long long kstep = (unsigned long long)fv.fstride << kKeyShift;
+      Key* dst = keys + cell_off + base + (uniform ? rank : prefix);
+      if constexpr (kWide) {
+        const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
+        const unsigned long long kstep = (unsigned long long)fv.fstride << kKeyShift;
 #pragma unroll
-      for (int t = 0; t < kMaxRun; ++t) {
-        if ((uint32_t)t < k) {
-          *dst = key0 + (unsigned long long)t * kstep + (((bb >> (2 * t)) & 3u) << 8) + inten[t];
-          dst += stride;
+        for (int t = 0; t < kMaxRun; ++t) {
+          if ((uint32_t)t < k) {
+            *dst = key0 + (unsigned long long)t * kstep + (((bb >> (2 * t)) & 3u) << 8) + inten[t];
+            dst += stride;
+          }
+        }
+      } else {
+        const uint32_t key0 = ((f0 + run_j) * fv.fstride + pk) << 2;
+#pragma unroll
+        for (int t = 0; t < kMaxRun; ++t) {
+          if ((uint32_t)t < k) {
+            *dst = key0 + ((uint32_t)t * fv.fstride << 2) + ((bb >> (2 * t)) & 3u);
+            dst += stride;
+          }
         }
       }
     }
@@ -448,14 +467,14 @@ __global__ void __launch_bounds__(256) sample_scatter_k(const float* __restrict_
 struct __align__(32) SealAxes {
   double r0x, r0y, r1x, r1y;  // load A
   double r2x, r2y, t0, t1;    // load B
-  double t2;                  // load C: t2 | oid
-  uint32_t oid, pad;
+  double t2;                  // load C: t2 | oid | image
+  uint32_t oid, image;
   double pad2[2];
 };
 static_assert(sizeof(SealAxes) == 96, "SealAxes layout");
 
 __global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __restrict__ oid,
-                            uint32_t n, SealAxes* out) {
+                            const int32_t* __restrict__ image, uint32_t n, SealAxes* out) {
   const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
   const double* fa = axes + (size_t)f * 9;
@@ -470,7 +489,7 @@ __global__ void seal_axes_k(const double* __restrict__ axes, const uint32_t* __r
   x.t1 = fa[7];
   x.t2 = fa[8];
   x.oid = oid[f];
-  x.pad = 0;
+  x.image = (uint32_t)image[f];
   x.pad2[0] = x.pad2[1] = 0.0;
   out[f] = x;
 }
@@ -487,7 +506,11 @@ __device__ __forceinline__ void ld256_f64(const void* p, double& a, double& b, d
 }
 
 struct FrameRecords {
+  using Key = unsigned long long;
   static constexpr bool kKeyBins = true;  // z bins computed by the fill pass
+  __device__ static uint32_t key_pid(Key k) { return (uint32_t)(k >> kKeyShift); }
+  __device__ static uint32_t key_bin(Key k) { return (uint32_t)(k >> 8) & 3u; }
+  __device__ static uint32_t key_byte(Key k) { return (uint32_t)(k & 0xffu); }
   FrameView fv;
   const SealAxes* sa;
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t inten) const {
@@ -517,8 +540,50 @@ struct FrameRecords {
   }
 };
 
+// 32-bit keys (insertion index only): the intensity is read from the frame
+// (the seal visits cells z-chunk-major, so the frames of the concurrently
+// sealed cells are a small L2-resident band) and z is binned from the
+// recomputed position.
+struct FrameRecords32 {
+  using Key = uint32_t;
+  static constexpr bool kKeyBins = true;  // key = insertion index << 2 | z bin
+  __device__ static uint32_t key_pid(Key k) { return k >> 2; }
+  __device__ static uint32_t key_bin(Key k) { return k & 3u; }
+  __device__ static uint32_t key_byte(Key) { return 0u; }
+  FrameView fv;
+  const SealAxes* sa;
+  __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t) const {
+    uint32_t f, u, v;
+    fv.decode(pid, f, u, v);
+    const SealAxes* x = sa + f;
+    double r0x, r0y, r1x, r1y, r2x, r2y, t0, t1;
+    ld256_f64(&x->r0x, r0x, r0y, r1x, r1y);
+    ld256_f64(&x->r2x, r2x, r2y, t0, t1);
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(&x->t2));
+    const uint32_t inten = __ldg(fv.frames + (size_t)c.w * fv.hw + v * fv.W + u);
+    const double t2 = __hiloint2double((int)c.y, (int)c.x);
+    const double U = (double)u * fv.px, V = (double)v * fv.py;
+    // reconstruct.py:156-162: ((U*R[a,0]) + (V*R[a,1])) + t[a]
+    const float p0 = __double2float_rn((U * r0x + V * r0y) + t0);
+    const float p1 = __double2float_rn((U * r1x + V * r1y) + t1);
+    const float p2 = __double2float_rn((U * r2x + V * r2y) + t2);
+    return make_uint4(__float_as_uint(p0), __float_as_uint(p1), __float_as_uint(p2), (c.z << 8) | inten);
+  }
+  __device__ __forceinline__ float z_of(uint32_t pid) const {
+    uint32_t f, u, v;
+    fv.decode(pid, f, u, v);
+    const SealAxes& x = sa[f];
+    const double U = (double)u * fv.px, V = (double)v * fv.py;
+    return __double2float_rn((U * x.r2x + V * x.r2y) + x.t2);
+  }
+};
+
 struct SampleRecords {
+  using Key = unsigned long long;
   static constexpr bool kKeyBins = false;
+  __device__ static uint32_t key_pid(Key k) { return (uint32_t)(k >> kKeyShift); }
+  __device__ static uint32_t key_bin(Key) { return 0u; }
+  __device__ static uint32_t key_byte(Key k) { return (uint32_t)(k & 0xffu); }
   const float* pos;
   const uint32_t* word;  // (oid << 8) | intensity
   __device__ __forceinline__ uint4 operator()(uint32_t pid, uint32_t) const {
@@ -568,7 +633,7 @@ struct BinOut {
 template <class Rec, int kRun>
 __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(Rec rec,
                                                           const uint32_t* __restrict__ offsets,
-                                                          const unsigned long long* __restrict__ keys,
+                                                          const typename Rec::Key* __restrict__ keys,
                                                           uint32_t ncells, uint4* records,
                                                           uint32_t* big_cells, uint32_t* n_big,
                                                           BinOut bo) {
@@ -607,11 +672,11 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     // warps.  Four loads in flight per lane; keys are read once (streaming, L1
     // kept for the frame-axes lookups of the record pass)
     for (uint32_t i0 = 0; i0 < len; i0 += 128) {
-      unsigned long long kk[4];
+      typename Rec::Key kk[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t i = i0 + 32u * q + lane;
-        kk[q] = i < len ? __ldcs(keys + s0 + i) : 0ull;
+        kk[q] = i < len ? __ldcs(keys + s0 + i) : (typename Rec::Key)0;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -619,16 +684,16 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
         if (i < len) {
           const uint32_t pw = sm.pos_of[i], col = pw & 31u;
           const uint32_t at = stage_at(pw >> 5, col);
-          const uint32_t pid = (uint32_t)(kk[q] >> kKeyShift);
+          const uint32_t pid = Rec::key_pid(kk[q]);
           uint32_t bin;
           if constexpr (Rec::kKeyBins) {
-            bin = (uint32_t)(kk[q] >> 8) & 3u;
+            bin = Rec::key_bin(kk[q]);
           } else {
             const float z = rec.z_of(pid);
             bin = (z >= sm.zb[0][col]) + (z >= sm.zb[1][col]) + (z >= sm.zb[2][col]);
           }
           sm.st[at] = pid;
-          sm.sx[at] = (uint16_t)((kk[q] & 0xffu) | (bin << 8));
+          sm.sx[at] = (uint16_t)(Rec::key_byte(kk[q]) | (bin << 8));
         }
       }
     }
@@ -675,9 +740,9 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     }
   } else if (cn > 0 && !big) {
     // a big run in this warp's chunk: the small runs are sealed lane by lane
-    unsigned long long k[kRun];
+    typename Rec::Key k[kRun];
     for (uint32_t i = 0; i < cn; ++i) {
-      const unsigned long long x = keys[cs + i];
+      const typename Rec::Key x = keys[cs + i];
       uint32_t j = i;
       while (j > 0 && k[j - 1] > x) {
         k[j] = k[j - 1];
@@ -686,7 +751,7 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
       k[j] = x;
     }
     for (uint32_t i = 0; i < cn; ++i) {
-      records[cs + i] = rec((uint32_t)(k[i] >> kKeyShift), (uint32_t)(k[i] & 0xffu));
+      records[cs + i] = rec(Rec::key_pid(k[i]), Rec::key_byte(k[i]));
       bo.perm[cs + i] = 0;
     }
   }
@@ -710,10 +775,10 @@ __global__ void big_bounds_k(const uint32_t* big_cells, uint32_t n_big,
 // block per big cell: records from the segment-sorted keys
 template <class Rec>
 __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_t* ends,
-                                  const unsigned long long* __restrict__ sorted, uint4* records) {
+                                  const typename Rec::Key* __restrict__ sorted, uint4* records) {
   uint32_t b = begins[blockIdx.x], e = ends[blockIdx.x];
   for (uint32_t s = b + threadIdx.x; s < e; s += blockDim.x)
-    records[s] = rec((uint32_t)(sorted[s] >> kKeyShift), (uint32_t)(sorted[s] & 0xffu));
+    records[s] = rec(Rec::key_pid(sorted[s]), Rec::key_byte(sorted[s]));
 }
 
 // count -> scan -> fill -> seal, shared by frames and arbitrary samples.
@@ -728,7 +793,8 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   DARE_CUDA(cudaMemsetAsync(rej.ptr, 0, sizeof(unsigned long long), s));
   dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
   pt.mark("alloc+memset");
-  scatter(false, counts.ptr, (const uint32_t*)nullptr, (unsigned long long*)nullptr, rej.ptr);
+  using Key = typename Rec::Key;
+  scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
   size_t tmp_bytes = 0, max_bytes = 0;
@@ -759,10 +825,10 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     DARE_CUDA(cudaMemsetAsync(vol->d_bins, 0, sizeof(uint32_t) * std::max<int64_t>(ncells, 1), s));
     return;
   }
-  Scratch<unsigned long long> keys(n_kept, s);
+  Scratch<Key> keys(n_kept, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncells, s));
   pt.mark("readback+alloc");
-  scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, keys.ptr,
+  scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr,
           (unsigned long long*)nullptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("fill");
@@ -791,7 +857,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   if (n_big == 0) return;
   DARE_LIMIT(n_kept < (uint32_t)INT32_MAX, "segmented sort limited to 2^31 samples");
   Scratch<uint32_t> begins(n_big, s), ends(n_big, s);
-  Scratch<unsigned long long> sorted(n_kept, s);
+  Scratch<Key> sorted(n_kept, s);
   big_bounds_k<<<ceil_div(n_big, 256), 256, 0, s>>>(big_cells, n_big, vol->d_offsets,
                                                     begins.ptr, ends.ptr);
   size_t sort_bytes = 0;
@@ -882,12 +948,19 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     CellTables ct;
     const char* legacy = getenv("DARE_COUNT_LEGACY");
     const bool tabs_ok = !(legacy && legacy[0] == '1') && build_cell_tables(m, true, s, tab_store, ct);
-    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
-                       unsigned long long* keys, unsigned long long* rej) {
+    // 32-bit keys when the packed (frame, v, u) insertion index fits
+    // (measured at cfg2: fill 1.09 -> 0.68 ms but seal 1.77 -> 2.36 ms from the
+    // intensity gather, so 64-bit keys stay the default; DARE_NARROW_KEYS=1 selects them)
+    const char* narrow_env = getenv("DARE_NARROW_KEYS");
+    const bool narrow_keys = fv.packed != 0 && fv.fshift + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 30 &&
+                             narrow_env && narrow_env[0] == '1';
+    const bool narrow = narrow_keys;
+    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
+                       unsigned long long* rej) {
       if (n_frames == 0) return;
       if (!fill) {  // needs no intensities: runs while host frames are still uploading
         if (tabs_ok)
-          frame_count_tab_k<<<dim3(tiles, chunks), 256, 0, s>>>(fv, ct, m, counts, runs.ptr, nruns.ptr, rej);
+          frame_count_tab_k<true><<<dim3(tiles, chunks), 256, 0, s>>>(fv, ct, m, counts, runs.ptr, nruns.ptr, rej);
         else
           (m.exact_inv ? frame_count_k<true> : frame_count_k<false>)<<<dim3(tiles, chunks), 256, 0, s>>>(
               fv, m, counts, runs.ptr, nruns.ptr, rej);
@@ -899,19 +972,27 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
       for (int64_t c0 = 0; c0 < (int64_t)chunks; c0 += step) {
         const int64_t c1 = std::min<int64_t>(chunks, c0 + step);
         fs.wait_frames(s, c0 * kRunFrames, std::min<int64_t>(n_frames, c1 * kRunFrames));
-        frame_fill_k<<<dim3(tiles, (unsigned)(c1 - c0)), 256, 0, s>>>(fv, (uint32_t)c0, runs.ptr, nruns.ptr,
-                                                                      counts, offsets, keys);
+        if (narrow)
+          frame_fill_k<uint32_t><<<dim3(tiles, (unsigned)(c1 - c0)), 256, 0, s>>>(
+              fv, (uint32_t)c0, runs.ptr, nruns.ptr, counts, offsets, (uint32_t*)keys);
+        else
+          frame_fill_k<unsigned long long><<<dim3(tiles, (unsigned)(c1 - c0)), 256, 0, s>>>(
+              fv, (uint32_t)c0, runs.ptr, nruns.ptr, counts, offsets, (unsigned long long*)keys);
       }
     };
     Scratch<SealAxes> sa((size_t)std::max<int64_t>(n_frames, 1), s);
     if (n_frames > 0) {
-      seal_axes_k<<<ceil_div(n_frames, 256), 256, 0, s>>>(fs.d_axes, d_oid.ptr, (uint32_t)n_frames, sa.ptr);
+      seal_axes_k<<<ceil_div(n_frames, 256), 256, 0, s>>>(fs.d_axes, d_oid.ptr, fs.d_image, (uint32_t)n_frames,
+                                                          sa.ptr);
       DARE_CUDA(cudaGetLastError());
     }
     // measured: cfg3 (8000 frames, 576 KB of axes) seal 52.3 -> 46.0 ms at 75%
     fs.start_upload();  // after the small uploads above (they would queue behind the frames)
-    build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s,
-              n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1);
+    const int carve = n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1;
+    if (narrow_keys)
+      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve);
+    else
+      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve);
     clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
@@ -950,15 +1031,15 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
     }
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
     const float* pos = d_pos.ptr;
-    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets,
-                       unsigned long long* keys, unsigned long long* rej) {
+    auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
+                       unsigned long long* rej) {
       if (n_samples == 0) return;
       if (fill)
-        sample_scatter_k<true><<<ceil_div(n_samples, 256), 256, 0, s>>>(pos, n_samples, m, counts,
-                                                                        offsets, keys, rej);
+        sample_scatter_k<true><<<ceil_div(n_samples, 256), 256, 0, s>>>(
+            pos, n_samples, m, counts, offsets, (unsigned long long*)keys, rej);
       else
-        sample_scatter_k<false><<<ceil_div(n_samples, 256), 256, 0, s>>>(pos, n_samples, m, counts,
-                                                                         offsets, keys, rej);
+        sample_scatter_k<false><<<ceil_div(n_samples, 256), 256, 0, s>>>(
+            pos, n_samples, m, counts, offsets, (unsigned long long*)keys, rej);
     };
     build_csr(vol.get(), SampleRecords{d_pos.ptr, d_word.ptr}, scatter, s);
     DARE_CUDA(cudaStreamSynchronize(s));
