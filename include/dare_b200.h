@@ -222,6 +222,13 @@ int dare_frame_poses(int64_t n, const double* mq, const double* mt, const double
                      const double* cal_t, int32_t width, int32_t height, double px, double py,
                      double* rot, double* trans, double* axes, float* quats32, double* lo,
                      double* hi, int32_t* status, int64_t* bad, double* bad_norm);
+/* Pose interpolation of synchronize() (reconstruct.py:102-116, slerp
+ * geometry.py:159-180) for n frames at times t[j] strictly inside the pose
+ * stream interval [ts[idx[j]], ts[idx[j]+1]] (idx = searchsorted(ts, t,
+ * "right") - 1, computed by the caller): marker quaternions out_q n x 4 and
+ * translations out_t n x 3, the reference's bits (host only, no device). */
+int dare_interpolate_poses(int64_t n, const double* t, const int64_t* idx, const double* ts,
+                           const double* pose_q, const double* pose_t, double* out_q, double* out_t);
 /* Service form of dare_reslice (service.py:273-293 process_request, which
  * reslices one request and ships protocol.pack_coverage(image.coverage),
  * protocol.py:273-274): same pixels; coverage bit-packed on the device per pose

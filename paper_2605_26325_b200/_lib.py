@@ -92,6 +92,7 @@ _SIGNATURES = {
     "dare_frame_poses": [c_i64, P_f64, P_f64, P_f64, P_f64, c_i32, c_i32, c_f64, c_f64, P_f64, P_f64, P_f64,
                          P_f32, P_f64, P_f64, ctypes.POINTER(c_i32), ctypes.POINTER(c_i64),
                          ctypes.POINTER(c_f64)],
+    "dare_interpolate_poses": [c_i64, P_f64, P_i64, P_f64, P_f64, P_f64, P_f64, P_f64],
     "dare_reslice": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_packed": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8, P_u8],
     "dare_reslice_bruteforce": [c_vp, c_i32, P_f64, c_i32, c_i32, ctypes.POINTER(ResliceCfg), P_u8,

@@ -135,3 +135,62 @@ extern "C" int dare_frame_poses(int64_t n, const double* mq, const double* mt, c
     }
   });
 }
+
+// Pose interpolation of synchronize() (reconstruct.py:102-116 interpolate_pose)
+// for the frames whose timestamp falls strictly between two pose samples:
+// alpha = (t - t0) / (t1 - t0) (0 when t1 == t0), translation
+// (1 - alpha) p0 + alpha p1 elementwise, rotation slerp (geometry.py:159-180).
+// numpy's dot of two 4-vectors (slerp's dot and linalg.norm's sum of
+// squares) evaluates, with the OpenBLAS tail loop it dispatches to on these
+// hosts, s = a0 b0, then s = fma(a_i, b_i, s) for i = 1..3 -- measured equal
+// on 200k random vectors, tests/test_host_logic.py -- so that is what is
+// restated here; acos / sin are the C library's, the functions Python's math
+// module calls.
+namespace {
+
+inline double np_dot4(const double* a, const double* b) {
+  double s = a[0] * b[0];
+  s = std::fma(a[1], b[1], s);
+  s = std::fma(a[2], b[2], s);
+  s = std::fma(a[3], b[3], s);
+  return s;
+}
+
+void slerp(const double* q0, const double* q1, double t, double* out) {
+  double b[4] = {q1[0], q1[1], q1[2], q1[3]};
+  double dot = np_dot4(q0, b);
+  if (dot < 0.0) {
+    for (int k = 0; k < 4; ++k) b[k] = -b[k];
+    dot = -dot;
+  }
+  double o[4];
+  if (dot > 0.9995) {
+    for (int k = 0; k < 4; ++k) o[k] = q0[k] + t * (b[k] - q0[k]);
+  } else {
+    const double theta = std::acos(dot < 1.0 ? dot : 1.0);  // min(1.0, dot)
+    const double sin_theta = std::sin(theta);
+    const double w0 = std::sin((1.0 - t) * theta) / sin_theta;
+    const double w1 = std::sin(t * theta) / sin_theta;
+    for (int k = 0; k < 4; ++k) o[k] = w0 * q0[k] + w1 * b[k];
+  }
+  const double n = std::sqrt(np_dot4(o, o));  // np.linalg.norm
+  for (int k = 0; k < 4; ++k) out[k] = o[k] / n;
+}
+
+}  // namespace
+
+extern "C" int dare_interpolate_poses(int64_t n, const double* t, const int64_t* idx, const double* ts,
+                                      const double* pose_q, const double* pose_t, double* out_q,
+                                      double* out_t) {
+  return dare::guard([&] {
+    DARE_REQUIRE(n >= 0, "negative frame count");
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t i = idx[j];
+      const double t0 = ts[i], t1 = ts[i + 1];
+      const double alpha = t1 == t0 ? 0.0 : (t[j] - t0) / (t1 - t0);
+      slerp(pose_q + 4 * i, pose_q + 4 * (i + 1), alpha, out_q + 4 * j);
+      for (int k = 0; k < 3; ++k)
+        out_t[3 * j + k] = (1.0 - alpha) * pose_t[3 * i + k] + alpha * pose_t[3 * (i + 1) + k];
+    }
+  });
+}

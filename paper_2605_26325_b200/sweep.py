@@ -201,10 +201,20 @@ def plan_frames(sweep) -> FramePlan:
     all_t = _translation_array(poses)
     mq[exact] = all_q[idx[exact]]
     mt[exact] = all_t[idx[exact]]
-    for j in np.nonzero(~exact)[0]:
-        m = interpolate_pose(float(t[j]), ts, poses)
-        mq[j] = (m.rotation.w, m.rotation.x, m.rotation.y, m.rotation.z)
-        mt[j] = m.translation
+    interp = np.nonzero(~exact)[0]
+    if len(interp):  # slerp + lerp in one host call (csrc/plan.cu: dare_interpolate_poses)
+        from . import _lib
+
+        ti = np.ascontiguousarray(t[interp], dtype=np.float64)
+        ii = np.ascontiguousarray(idx[interp], dtype=np.int64)
+        oq = np.empty((len(interp), 4))
+        ot = np.empty((len(interp), 3))
+        P = ctypes.c_double
+        tsc = np.ascontiguousarray(ts, dtype=np.float64)
+        _lib.call("dare_interpolate_poses", len(interp), _lib.ptr(ti, P), _lib.ptr(ii, ctypes.c_int64),
+                  _lib.ptr(tsc, P), _lib.ptr(all_q, P), _lib.ptr(all_t, P), _lib.ptr(oq, P), _lib.ptr(ot, P))
+        mq[interp] = oq
+        mt[interp] = ot
 
     return _compose_plan(kept, mq, mt, sweep.calibration, dropped, (float(px), float(py)), int(height), int(width))
 

@@ -61,6 +61,22 @@ def _random_sweep(rng, n, h, w, pitch, spread):
     return db.SweepRecording(rng.integers(0, 256, (n, h, w), dtype=np.uint8), ts, ts, poses, pitch)
 
 
+@pytest.mark.parametrize("env", ["DARE_COUNT_LEGACY", "DARE_NARROW_KEYS"])
+@pytest.mark.parametrize("key", REC_KEYS)
+def test_reconstruct_alternative_passes_match_reference(golden, key, env, monkeypatch):
+    """The kept alternative passes (the FP64-chain count / compound kernels used
+    when a threshold table cannot be built, and 32-bit sort keys) give the same
+    bytes as the default path."""
+    monkeypatch.setenv(env, "1")
+    rec, voxel, margin = golden.sweep(key)
+    v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
+    assert_volume_equal(v, golden.volume(key + ".out"))
+    if key != "rec_drop":
+        s = db.compound(rec, voxel_size=voxel, margin=margin)
+        np.testing.assert_array_equal(s.values, golden[f"cmp_{key}.values"])
+        np.testing.assert_array_equal(s.counts, golden[f"cmp_{key}.counts"])
+
+
 @pytest.mark.parametrize("seed,voxel,margin", [(1, 0.25, 0.0), (2, 0.1, 0.5), (3, 0.37, 1.0)])
 def test_reconstruct_random_sweeps_match_oracle(seed, voxel, margin):
     rng = np.random.default_rng(seed)

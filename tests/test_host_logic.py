@@ -183,3 +183,50 @@ def test_frame_pose_pipeline_c_equals_numpy():
         S._compose_plan(kept, bad, mt, cal, 0, (0.1, 0.1), 4, 4)
     with pytest.raises(InvalidArgumentError, match="quaternion norm 1.010000 deviates"):
         S._compose_plan_numpy(kept, bad, mt, cal, 0, (0.1, 0.1), 4, 4)
+
+
+def test_interpolated_poses_c_equal_reference_formula():
+    """dare_interpolate_poses (csrc/plan.cu) == interpolate_pose's numpy/math
+    formula (reconstruct.py:102-116, slerp geometry.py:159-180) bit for bit:
+    random streams incl. near-parallel (nlerp branch) and antipodal neighbours,
+    repeated timestamps; 8000 interpolated frames in well under a second."""
+    import time
+
+    from paper_2605_26325_b200 import sweep as S
+
+    rng = np.random.default_rng(17)
+    m = 900
+    ts = np.cumsum(rng.uniform(0.0, 0.03, m))
+    ts[100:103] = ts[100]  # t1 == t0 brackets
+    q = rng.normal(size=(m, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[1::3] = q[0::3][: len(q[1::3])] + rng.normal(scale=1e-3, size=(len(q[1::3]), 4))  # nearly parallel
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[2::5] *= -1.0  # antipodal sign flips
+    poses = [Pose(Quaternion(*qq), rng.uniform(-5, 5, 3)) for qq in q]
+    t_img = np.sort(np.concatenate([rng.uniform(ts[0], ts[-1], 7950), ts[:50]]))  # incl. exact timestamps
+    images = np.zeros((len(t_img), 2, 2), np.uint8)
+    rec = SweepRecording(images, t_img, ts, poses, (0.1, 0.1))
+    t0 = time.perf_counter()
+    plan = plan_frames(rec)
+    dt = time.perf_counter() - t0
+    assert dt < 1.0, dt
+    for j in range(0, len(t_img), 7):
+        ref = S.interpolate_pose(float(t_img[j]), ts, poses).compose(Pose.identity())
+        np.testing.assert_array_equal(plan.rotations[j], [ref.rotation.w, ref.rotation.x, ref.rotation.y,
+                                                          ref.rotation.z])
+        np.testing.assert_array_equal(plan.translations[j], ref.translation)
+
+
+def test_numpy_dot4_is_the_fma_chain():
+    """The restatement's premise: numpy's dot of two 4-vectors (slerp, norm) is
+    a0 b0 then fma(a_i, b_i, s) on this host (checked exactly with fractions)."""
+    from fractions import Fraction as F
+
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        a, b = rng.normal(size=4), rng.normal(size=4)
+        s = a[0] * b[0]
+        for i in (1, 2, 3):
+            s = float(F(a[i]) * F(b[i]) + F(s))
+        assert s == float(np.dot(a, b))
