@@ -67,6 +67,13 @@ struct FrameView {
   // when the bit widths fit 32 bits -- same order as f * hw + v * W + u, decoded
   // with shifts in the seal -- else linear (f * hw + p, decoded with FastDiv)
   uint32_t packed, ushift, fshift, fstride;
+  // frame groups of the count / fill passes (see build_csr): chunk k of 64
+  // frames belongs to group k / chunks_per_group, whose per-cell counters and
+  // key offsets live at + group * ncells
+  uint32_t chunks_per_group, ncells;
+  __device__ __forceinline__ size_t group_base(uint32_t chunk) const {
+    return (size_t)(chunk / chunks_per_group) * ncells;
+  }
   __device__ __forceinline__ uint32_t pixel_key(uint32_t u, uint32_t v) const {
     return packed ? (v << ushift) | u : v * W + u;
   }
@@ -83,6 +90,10 @@ struct FrameView {
     }
   }
 };
+
+static inline bool ncells_total_fits(int64_t ncells, int64_t groups) {
+  return ncells * groups < (int64_t)UINT32_MAX - 1;
+}
 
 static inline uint32_t ceil_log2(uint64_t x) {
   uint32_t l = 0;
@@ -187,6 +198,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
   __syncthreads();
   const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
+  counts += fv.group_base(blockIdx.y);
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   int32_t cur = -1;
   uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_oob = 0;
@@ -262,6 +274,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
   __syncthreads();
   const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
+  counts += fv.group_base(blockIdx.y);
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
   AxisCell ax[2];
@@ -366,6 +379,8 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
   const size_t blk = (size_t)chunk * gridDim.x + blockIdx.x;
   const uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const uint32_t nr = nruns[blk * 256 + threadIdx.x];
+  counts += fv.group_base(chunk);
+  offsets += fv.group_base(chunk);
   const uint32_t max_nr = __reduce_max_sync(0xffffffffu, nr);
   uint2 next = nr > 0 ? my[0] : make_uint2(0u, 0u);
   for (uint32_t r = 0; r < max_nr; ++r) {
@@ -781,32 +796,101 @@ __global__ void big_materialize_k(Rec rec, const uint32_t* begins, const uint32_
     records[s] = rec(Rec::key_pid(sorted[s]), Rec::key_byte(sorted[s]));
 }
 
+// Frame-grouped keys (groups > 1): the count / fill passes keep one CSR of
+// keys per group of frames (group-major: koff[g * ncells + c]), so that the
+// fill of a group -- a contiguous frame range, typically one sweep direction
+// -- writes each cell's keys in one visit, into memory its neighbouring cells'
+// keys share; with one CSR for every frame, multi-direction sweeps (cfg3: four
+// sweeps) visit each cell's 32 B of keys four times far apart in time and L2
+// merges the partial sectors in DRAM (67 GB of traffic for 16.8 GB of keys).
+// The regroup pass then lays the keys out cell-major for the seal: warp per 32
+// consecutive cells, per group one coalesced segment read, written into the
+// cells' final ranges (a contiguous window per warp, fully written at once).
+__global__ void group_totals_k(const uint32_t* __restrict__ koff, uint32_t ncells, uint32_t groups,
+                               uint32_t* totals) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  uint32_t t = 0;
+  for (uint32_t g = 0; g < groups; ++g) {
+    const size_t i = (size_t)g * ncells + c;
+    t += koff[i + 1] - koff[i];
+  }
+  totals[c] = t;
+}
+
+template <class Key>
+__global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict__ koff,
+                                                      const uint32_t* __restrict__ offsets, uint32_t ncells,
+                                                      uint32_t groups, const Key* __restrict__ in, Key* out) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  const uint32_t c0 = warp * 32u;
+  if (c0 >= ncells) return;  // warp-uniform
+  const uint32_t c = c0 + lane, c_end = min(c0 + 32u, ncells);
+  uint32_t dst = c < c_end ? offsets[c] : 0u;  // this lane's cell: next free output slot
+  for (uint32_t g = 0; g < groups; ++g) {
+    const size_t base = (size_t)g * ncells;
+    const uint32_t seg0 = koff[base + c0], seg1 = koff[base + c_end];
+    const uint32_t my0 = c < c_end ? koff[base + c] : seg1;
+    const uint32_t my1 = c < c_end ? koff[base + c + 1] : seg1;
+    for (uint32_t i0 = seg0; i0 < seg1; i0 += 32) {  // warp-uniform trip count
+      const uint32_t i = i0 + lane;
+      // owner of key i: the last lane whose cell starts at or before i
+      int lo = 0, hi = 31;
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        const int mid = (lo + hi + 1) >> 1;
+        const uint32_t m0 = __shfl_sync(0xffffffffu, my0, mid);
+        if (m0 <= i) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint32_t o_start = __shfl_sync(0xffffffffu, my0, lo);
+      const uint32_t o_dst = __shfl_sync(0xffffffffu, dst, lo);
+      if (i < seg1) out[o_dst + (i - o_start)] = __ldcs(in + i);
+    }
+    dst += my1 - my0;
+  }
+}
+
 // count -> scan -> fill -> seal, shared by frames and arbitrary samples.
 // `scatter(fill, counts, offsets, keys, rejected)` launches the source's pass.
 template <class Rec, class Scatter>
-void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int seal_carveout = -1) {
+void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int seal_carveout = -1,
+               uint32_t groups = 1) {
   const int64_t ncells = vol->ncells;
+  const int64_t nkc = ncells * (int64_t)groups;  // per-group counters (groups > 1: frame-grouped keys)
+  DARE_LIMIT(nkc < (int64_t)UINT32_MAX, "too many cells x frame groups");
   PhaseTimer pt(s, "build_csr");
-  Scratch<uint32_t> counts(ncells + 1, s);
+  Scratch<uint32_t> counts(nkc + 1, s);
   Scratch<unsigned long long> rej(1, s);
-  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (ncells + 1), s));
+  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (nkc + 1), s));
   DARE_CUDA(cudaMemsetAsync(rej.ptr, 0, sizeof(unsigned long long), s));
   dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
+  Scratch<uint32_t> koff(groups > 1 ? nkc + 1 : 0, s);
+  Scratch<uint32_t> totals(groups > 1 ? ncells + 1 : 0, s);
   pt.mark("alloc+memset");
   using Key = typename Rec::Key;
   scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
-  size_t tmp_bytes = 0, max_bytes = 0;
+  size_t tmp_bytes = 0, max_bytes = 0, tmp2_bytes = 0;
   Scratch<uint32_t> max_d(1, s);
-  DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.ptr, vol->d_offsets,
-                                          ncells + 1, s));
-  DARE_CUDA(cub::DeviceReduce::Max(nullptr, max_bytes, counts.ptr, max_d.ptr, ncells, s));
+  // per-cell totals: the counters themselves (one group) or their sum over groups
+  uint32_t* tot = counts.ptr;
+  if (groups > 1) {
+    DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2_bytes, counts.ptr, koff.ptr, nkc + 1, s));
+    Scratch<uint8_t> tmp(tmp2_bytes, s);
+    DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp2_bytes, counts.ptr, koff.ptr, nkc + 1, s));
+    group_totals_k<<<ceil_div(ncells, 256), 256, 0, s>>>(koff.ptr, (uint32_t)ncells, groups, totals.ptr);
+    DARE_CUDA(cudaGetLastError());
+    DARE_CUDA(cudaMemsetAsync(totals.ptr + ncells, 0, sizeof(uint32_t), s));
+    tot = totals.ptr;
+  }
+  DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tot, vol->d_offsets, ncells + 1, s));
+  DARE_CUDA(cub::DeviceReduce::Max(nullptr, max_bytes, tot, max_d.ptr, ncells, s));
   {
     Scratch<uint8_t> tmp(std::max(tmp_bytes, max_bytes), s);
-    DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, counts.ptr, vol->d_offsets,
-                                            ncells + 1, s));
-    DARE_CUDA(cub::DeviceReduce::Max(tmp.ptr, max_bytes, counts.ptr, max_d.ptr, ncells, s));
+    DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, tot, vol->d_offsets, ncells + 1, s));
+    DARE_CUDA(cub::DeviceReduce::Max(tmp.ptr, max_bytes, tot, max_d.ptr, ncells, s));
   }
   pt.mark("scan");
   uint32_t n_kept = 0, max_run = 0;
@@ -826,12 +910,22 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     return;
   }
   Scratch<Key> keys(n_kept, s);
-  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncells, s));
+  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * nkc, s));
   pt.mark("readback+alloc");
-  scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr,
-          (unsigned long long*)nullptr);
-  DARE_CUDA(cudaGetLastError());
-  pt.mark("fill");
+  if (groups > 1) {
+    Scratch<Key> gkeys(n_kept, s);
+    scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr);
+    DARE_CUDA(cudaGetLastError());
+    pt.mark("fill");
+    regroup_keys_k<Key><<<ceil_div(ceil_div(ncells, 32) * 32, 256), 256, 0, s>>>(
+        koff.ptr, vol->d_offsets, (uint32_t)ncells, groups, gkeys.ptr, keys.ptr);
+    DARE_CUDA(cudaGetLastError());
+    pt.mark("regroup");
+  } else {
+    scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr, (unsigned long long*)nullptr);
+    DARE_CUDA(cudaGetLastError());
+    pt.mark("fill");
+  }
   uint32_t* big_cells = counts.ptr;  // reuse: #big runs <= ncells
   Scratch<uint32_t> n_big_d(1, s);
   DARE_CUDA(cudaMemsetAsync(n_big_d.ptr, 0, sizeof(uint32_t), s));
@@ -920,7 +1014,8 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                               cudaMemcpyHostToDevice, s));
     FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
                  (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
-                 FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw};
+                 FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw,
+                 0xffffffffu, (uint32_t)vol->ncells};
     {
       const uint32_t ub = ceil_log2((uint64_t)width), vb = ceil_log2((uint64_t)height);
       if (ub + vb + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 32 && ub + vb < 32) {
@@ -989,10 +1084,26 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     // measured: cfg3 (8000 frames, 576 KB of axes) seal 52.3 -> 46.0 ms at 75%
     fs.start_upload();  // after the small uploads above (they would queue behind the frames)
     const int carve = n_frames * (int64_t)sizeof(SealAxes) > (128 << 10) ? 75 : -1;
+    // frame groups for the keys (see group_totals_k), a multiple of the 64-frame
+    // chunk each.  Measured at cfg3 (8 groups): fill 35 -> 26 ms, but the
+    // regroup (11.7 ms), the per-group counters and scans cost more -- the cfg3
+    // fill is bound by its ~525M returning atomics (one pixel per cell and
+    // sweep, so no lane aggregation), not by the partial sectors alone.  One
+    // group by default; DARE_KEY_GROUPS=n selects the grouped layout.
+    uint32_t groups = 1;
+    {
+      const char* genv = getenv("DARE_KEY_GROUPS");
+      const int64_t want = genv ? atoi(genv) : 1;
+      if (want > 1 && ncells_total_fits(vol->ncells, want)) {
+        const uint32_t cpg = (uint32_t)ceil_div(ceil_div(n_frames, want), kRunFrames);
+        fv.chunks_per_group = cpg;
+        groups = (uint32_t)ceil_div(ceil_div(n_frames, kRunFrames), cpg);
+      }
+    }
     if (narrow_keys)
-      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve);
+      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups);
     else
-      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve);
+      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups);
     clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;

@@ -61,20 +61,42 @@ def _random_sweep(rng, n, h, w, pitch, spread):
     return db.SweepRecording(rng.integers(0, 256, (n, h, w), dtype=np.uint8), ts, ts, poses, pitch)
 
 
-@pytest.mark.parametrize("env", ["DARE_COUNT_LEGACY", "DARE_NARROW_KEYS"])
+@pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
+                                       ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7")])
 @pytest.mark.parametrize("key", REC_KEYS)
-def test_reconstruct_alternative_passes_match_reference(golden, key, env, monkeypatch):
+def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
-    when a threshold table cannot be built, and 32-bit sort keys) give the same
-    bytes as the default path."""
-    monkeypatch.setenv(env, "1")
+    when a threshold table cannot be built, 32-bit sort keys, and frame-grouped
+    keys with the regroup pass -- the default for sweeps over ~1000 frames)
+    give the same bytes as the default path."""
+    monkeypatch.setenv(env, value)
     rec, voxel, margin = golden.sweep(key)
     v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
     assert_volume_equal(v, golden.volume(key + ".out"))
-    if key != "rec_drop":
+    if key != "rec_drop" and env != "DARE_KEY_GROUPS":
         s = db.compound(rec, voxel_size=voxel, margin=margin)
         np.testing.assert_array_equal(s.values, golden[f"cmp_{key}.values"])
         np.testing.assert_array_equal(s.counts, golden[f"cmp_{key}.counts"])
+
+
+@pytest.mark.parametrize("groups", ["0", "2", "3", "5"])
+def test_reconstruct_frame_grouped_keys_match_oracle(groups, monkeypatch):
+    """Multi-direction sweep of 330 frames (three sub-sweeps at different probe
+    orientations over one region, like cfg3) with the keys kept per frame
+    group and regrouped cell-major (DARE_KEY_GROUPS; 0 = the default choice)."""
+    if groups != "0":
+        monkeypatch.setenv("DARE_KEY_GROUPS", groups)
+    rng = np.random.default_rng(44)
+    poses = []
+    for k in range(330):
+        base = [Quaternion.identity(), Quaternion.from_axis_angle((0, 1, 0), 1.2),
+                Quaternion.from_axis_angle((1, 0, 0), -1.0)][k // 110]
+        s_ = (k % 110) * 0.02
+        poses.append(Pose(base, [(0.0, 0.0, s_), (s_, 0.0, 2.0), (0.0, s_, 2.0)][k // 110]))
+    ts = np.arange(330) / 30.0
+    rec = db.SweepRecording(rng.integers(0, 256, (330, 21, 23), dtype=np.uint8), ts, ts, poses, (0.1, 0.1))
+    v = db.reconstruct_volume(rec, voxel_size=0.1, margin=0.2)
+    assert_volume_equal(v, oracle.reconstruct(rec, 0.1, 0.2))
 
 
 @pytest.mark.parametrize("seed,voxel,margin", [(1, 0.25, 0.0), (2, 0.1, 0.5), (3, 0.37, 1.0)])
