@@ -1,0 +1,14 @@
+#!/bin/bash
+# Conformance run (GPU box): the reference's own hot-path test files, unmodified,
+# against this repo's drop-in (tests/conformance/dare_dropin.py).  Needs the
+# reference installed under baseline/_ref (pip --target, git-ignored) with its
+# test files copied to baseline/_ref/dare_tests (done in the build container).
+R=$(cd "$(dirname "$0")/.." && pwd)
+mkdir -p "$R/gpurun_out"
+cd "$R/baseline/_ref/dare_tests" || { echo "no baseline/_ref/dare_tests"; exit 2; }
+export PYTHONPATH="$R/baseline/_ref:$R:$R/tests/conformance:$PYTHONPATH" NUMBA_CACHE_DIR=/tmp/numba_cache
+# deselected: SSIM / scikit-image (absent from the image), the protocol golden
+# .bin files (absent from the reference mount), the node bridge
+DESEL="not ssim and not criterion_8 and not structural"
+timeout 1800 python -m pytest -p dare_dropin -q -p no:cacheprovider -rfE --rootdir . \
+  test_reconstruct.py test_reslice.py test_baseline.py test_volume.py test_acceptance.py -k "$DESEL" "$@"
