@@ -13,6 +13,8 @@ the package __init__):
   compound / fill_holes / reslice_trilinear (baseline.py:64-155)
                                                 -> paper_2605_26325_b200.scalar.*
 
+The service module's isinstance test of the volume kind (service.py:32,202)
+is widened to accept the drop-in's DirectionalVolume.
 reslice_bruteforce stays the reference's numba kernel, so the reference's
 oracle-equivalence tests (test_reslice.py:152-179, acceptance criterion 1)
 compare the GPU path against the reference's own brute force.  Test files are
@@ -58,6 +60,7 @@ def pytest_configure(config):
     import dare.reconstruct
     import dare.reslice
     import dare.service
+    import dare.volume
 
     import paper_2605_26325_b200 as b200
     from paper_2605_26325_b200 import _lib, scalar
@@ -76,6 +79,19 @@ def pytest_configure(config):
             if hasattr(mod, name):
                 setattr(mod, name, fn)
                 PATCHED.setdefault(mod.__name__, []).append(name)
+    # service.py:32 imported DirectionalVolume by value and tests the volume kind
+    # with isinstance (service.py:202): accept the drop-in's volumes as well
+    import abc
+
+    from paper_2605_26325_b200.volume import DirectionalVolume as B200Volume
+
+    class AnyDirectionalVolume(abc.ABC):
+        pass
+
+    AnyDirectionalVolume.register(dare.volume.DirectionalVolume)
+    AnyDirectionalVolume.register(B200Volume)
+    dare.service.DirectionalVolume = AnyDirectionalVolume
+    PATCHED.setdefault("dare.service", []).append("DirectionalVolume (isinstance accepts the drop-in's)")
     config.addinivalue_line("markers", "dropin: conformance run against the B200 drop-in")
 
 
