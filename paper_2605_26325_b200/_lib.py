@@ -17,6 +17,8 @@ from .errors import InvalidArgumentError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdare_b200.so")
+if os.environ.get("DARE_CHECKED") == "1":  # bounds-asserting build (build.py --checked), for test runs
+    LIB_PATH = os.path.join(_HERE, "libdare_b200_checked.so")
 
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64

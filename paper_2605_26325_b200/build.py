@@ -18,6 +18,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdare_b200.so")
+LIB_CHECKED = os.path.join(HERE, "libdare_b200_checked.so")  # -DDARE_CHECKED: device bounds asserts
 SOURCES = ["runtime.cu", "reconstruct.cu", "volume_api.cu", "reslice.cu", "scalar.cu", "merge.cu", "bins.cu",
            "plan.cu", "cells.cu"]
 HEADERS = ["common.cuh", "volume.cuh", "cells.cuh", "dare_exp.h", "exp_table.h"]
@@ -30,22 +31,25 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "dare_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """libdare_b200.so (or, with checked=True, libdare_b200_checked.so: the same
+    sources with -DDARE_CHECKED device-side bounds asserts, for test runs)."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
     nvcc = nvcc_path()
     objs = []
-    build_dir = os.path.join(HERE, "_build")
+    build_dir = os.path.join(HERE, "_build_checked" if checked else "_build")
     os.makedirs(build_dir, exist_ok=True)
     common = [
         "-gencode", "arch=compute_100a,code=sm_100a",
@@ -56,6 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     ]
     if verbose:
         common += ["-Xptxas", "-v"]
+    if checked:
+        common += ["-DDARE_CHECKED"]
     procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
@@ -72,14 +78,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write("FAILED: " + " ".join(cmd) + "\n")
     if failed:
         raise RuntimeError("nvcc compilation failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
             "-lcudart"]
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -165,6 +165,24 @@ inline void dev_alloc(T** p, size_t bytes) {
 
 // ---- device helpers ------------------------------------------------------
 
+// Checked build (build.py --checked -> libdare_b200_checked.so, loaded with
+// DARE_CHECKED=1): device-side bounds / invariant asserts at the hot kernels'
+// global and shared-memory accesses; a failure prints the condition and traps
+// (the launch fails, the tests report it).  No code in the default build.
+#ifdef DARE_CHECKED
+#define DARE_CHECK(cond)                                                                  \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("DARE_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);                \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define DARE_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // The reference's voxel-index chain `floor((f64(p32) - origin) / voxel)`
 // (volume.py:209).  When voxel is a power of two the division is replaced by
 // the exact reciprocal multiply (identical result, far cheaper on the FP64 pipe).

@@ -55,6 +55,7 @@ __global__ void merge_copy_k(MergeParts p, int64_t ncells, const uint32_t* __res
     for (uint32_t j = s + lane; j < e; j += 32) {
       uint4 rec = p.records[r][perm ? canon_to_store(perm, j) : j];
       rec.w = (__ldg(remap + (rec.w >> 8)) << 8) | (rec.w & 0xffu);
+      DARE_CHECK(dst + (j - s) < out_off[c + 1] && (rec.w >> 8) < (1u << 24));
       out[dst + (j - s)] = rec;
     }
     dst += e - s;

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
     const int32_t lin = in_frame ? tracked : -1;
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     if (restart && cur >= 0) {
+      DARE_CHECK(nr < (uint32_t)kRunFrames && (uint32_t)cur < fv.ncells);
       atomicAdd(&counts[cur], k);
       my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
       ++nr;
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
       const uint32_t stride = uniform ? n : 1u;
+      DARE_CHECK(base + total <= offsets[lin + 1] - cell_off);
       Key* dst = keys + cell_off + base + (uniform ? rank : prefix);
       if constexpr (kWide) {
         const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
@@ -675,6 +677,7 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
   if (big) big_cells[atomicAdd(n_big, 1u)] = c;
   const uint32_t len = s1 - s0;
   const bool staged = !__any_sync(0xffffffffu, big);  // then len <= 32 * 32
+  DARE_CHECK(!staged || len <= (uint32_t)kRun * 32u);
   if (staged) {
     for (uint32_t k = 0; k < cn; ++k) sm.pos_of[cs - s0 + k] = (uint16_t)((k << 5) | lane);
     if constexpr (!Rec::kKeyBins) {
@@ -750,6 +753,7 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
     for (uint32_t i = lane; i < len; i += 32) {
       const uint32_t pw = sm.pos_of[i], col = pw & 31u, j = pw >> 5;
       const uint32_t w = sm.sx[stage_at(j, col)], dest = w >> 8;
+      DARE_CHECK(j < (uint32_t)kRun && dest < (uint32_t)kRun && s0 + i - j + dest < s1);
       records[s0 + i - j + dest] = rec(sm.st[stage_at(j, col)], w & 0xffu);
       bo.perm[s0 + i] = (int8_t)((int)dest - (int)j);
     }
@@ -845,6 +849,7 @@ __global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict
       }
       const uint32_t o_start = __shfl_sync(0xffffffffu, my0, lo);
       const uint32_t o_dst = __shfl_sync(0xffffffffu, dst, lo);
+      DARE_CHECK(i >= seg1 || (i >= o_start && o_dst + (i - o_start) < offsets[c_end]));
       if (i < seg1) out[o_dst + (i - o_start)] = __ldcs(in + i);
     }
     dst += my1 - my0;

@@ -451,6 +451,7 @@ struct FastWalk {
           // one contiguous storage range: drop the z quarters of the first and
           // last cell that lie wholly outside [zlo, zhi] (binned cells only)
           const int64_t base = ((int64_t)cx * a.dims[1] + cy) * a.dims[2];
+          DARE_CHECK(cx >= 0 && cy >= 0 && loz >= 0 && base + hiz + 1 <= a.dims[0] * a.dims[1] * a.dims[2]);
           const uint32_t o_lo = __ldg(a.offsets + base + loz);
           const uint32_t o_hi = __ldg(a.offsets + base + hiz);
           const uint32_t o_end = __ldg(a.offsets + base + hiz + 1);
@@ -501,6 +502,7 @@ template <int kDistMode, int kGate>
 __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
                                           const float* gate, float g_single, const float (&wh)[3],
                                           const float (&wl)[3], float c2, float& bw, float& bj) {
+  DARE_CHECK(!valid || kGate == kGateSingle || (c.w >> 8) < 1024u || kGate == kGateGlobal);
   const float g = kGate == kGateSingle ? g_single
                                        : (kGate == kGateSmem ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8)));
   // (single orientation: a gated-out pose never walks, see reslice_fast_k)
@@ -693,6 +695,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   while (live) {
     uint4 r[4];
     const uint32_t last_pair = (w.e - 1) >> 1;
+    DARE_CHECK(w.s < w.e && w.e <= a.n_samples && (i0 >> 1) <= last_pair);
     load_pair(a.records, i0 >> 1, r[0], r[1]);
     load_pair(a.records, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
     float bw = 0.0f, bj = 0.0f;
@@ -729,6 +732,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
                 fmax(fabs((pp[1] + du * pp[6]) + dv * pp[7]), fabs((pp[2] + du * pp[9]) + dv * pp[10])));
   }
   const size_t k = ((size_t)pose * a.H + v) * a.W + u;
+  DARE_CHECK(pose < a.P && k < (size_t)a.P * a.H * a.W);
   uint8_t ov, oc;
   if (certify(a, maxw, c2, W, J, visits, ov, oc)) {
     out[k] = ov;
@@ -798,6 +802,7 @@ __device__ __forceinline__ bool exact_sums_flat(const Walk& w, const ResliceArgs
       const uint32_t col_start = __shfl_sync(0xffffffffu, cs, lo);
       const uint32_t col_excl = __shfl_sync(0xffffffffu, incl - len, lo);
       in[t] = q < V;
+      DARE_CHECK(!in[t] || col_start + (q - col_excl) < a.n_samples);
       c[t] = in[t] ? __ldg(a.records + canon_to_store(a.perm, col_start + (q - col_excl)))
                    : make_uint4(0, 0, 0, 0);
     }
@@ -876,6 +881,7 @@ __global__ void __launch_bounds__(256) reslice_fallback_k(ResliceArgs a, uint8_t
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += warps) {
     const uint64_t k = all ? i : a.amb[i];
+    DARE_CHECK(k < (uint64_t)a.P * a.H * a.W);
     const int u = (int)(k % (uint64_t)a.W);
     const uint64_t t = k / (uint64_t)a.W;
     const int v = (int)(t % (uint64_t)a.H);

@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTa
     const bool ok = in_frame && ax[0].g >= 0 && ax[0].g < ct.n[0] && ax[1].g >= 0 && ax[1].g < ct.n[1] &&
                     ax[2].g >= 0 && ax[2].g < ct.n[2];
     const int32_t lin = ok ? (int32_t)(((uint32_t)ax[0].g * ny + (uint32_t)ax[1].g) * nz + (uint32_t)ax[2].g) : -1;
+    DARE_CHECK(lin < 0 || (int64_t)lin < m.dims[0] * m.dims[1] * m.dims[2]);
     const unsigned inten = in_frame ? (unsigned)fv.frames[s_img[j] + p] : 0u;
     const bool change = lin != cur;
     const bool need = change && cur >= 0;

@@ -16,6 +16,8 @@ def pytest_configure(config):
     from oracle import oracle
 
     cuda_build.build()
+    if os.environ.get("DARE_CHECKED") == "1":
+        cuda_build.build(checked=True)
     oracle.build()
 
 
