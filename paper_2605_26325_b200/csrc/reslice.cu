@@ -1325,8 +1325,6 @@ __global__ void pack_coverage_k(const uint8_t* __restrict__ cov, int64_t hw, int
 }
 
 constexpr size_t kStageMax = 4u << 20;  // outputs staged through pinned memory up to this size
-constexpr int32_t kOverlapChunk = 16;         // poses per launch when copies overlap compute
-constexpr size_t kOverlapMinPixels = 1u << 21;  // output size from which the overlap pays
 
 // host-buffer wrapper: params H2D, launches (<= 65535 poses each), outputs D2H
 // (coverage as bytes, or bit-packed per pose when `packed`)
@@ -1365,40 +1363,6 @@ static void reslice_host(dare_volume_t vol, int32_t n_poses, const double* param
     h_params = (const double*)h_stage;
   }
   DARE_CUDA(cudaMemcpyAsync(d_params, h_params, pbytes, cudaMemcpyHostToDevice, s));
-  // large batches into pinned host buffers: launched in pose chunks whose
-  // device->host copies (on the thread's copy stream) overlap the next chunk's
-  // kernels; only the last chunk's copy remains after the compute
-  const bool overlap = !stage && !packed && !brute && n_poses >= 2 * kOverlapChunk &&
-                       npix >= (size_t)kOverlapMinPixels && host_pinned(pixels) && host_pinned(coverage);
-  if (overlap) {
-    cudaStream_t cs = thread_copy_stream();
-    struct Events {
-      std::vector<cudaEvent_t> e;
-      ~Events() {
-        for (cudaEvent_t x : e) cudaEventDestroy(x);
-      }
-    } ev;
-    const size_t hw_px = (size_t)width * height;
-    for (int32_t p0 = 0; p0 < n_poses; p0 += kOverlapChunk) {
-      const int32_t np = std::min<int32_t>(kOverlapChunk, n_poses - p0);
-      const size_t off = (size_t)p0 * hw_px, bytes = (size_t)np * hw_px;
-      launch_reslice(vol, np, d_params + (size_t)p0 * 14, width, height, cfg, d_out + off, d_out + npix + off, s,
-                     brute, poses_coherent(params + (size_t)p0 * 14, np, width, height, vol->voxel), d_fb);
-      cudaEvent_t e;
-      DARE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ev.e.push_back(e);
-      DARE_CUDA(cudaEventRecord(e, s));
-      DARE_CUDA(cudaStreamWaitEvent(cs, e, 0));
-      DARE_CUDA(cudaMemcpyAsync(pixels + off, d_out + off, bytes, cudaMemcpyDeviceToHost, cs));
-      DARE_CUDA(cudaMemcpyAsync(coverage + off, d_out + npix + off, bytes, cudaMemcpyDeviceToHost, cs));
-    }
-    unsigned long long fb = 0;
-    DARE_CUDA(cudaMemcpyAsync(&fb, d_fb, sizeof(fb), cudaMemcpyDeviceToHost, s));
-    DARE_CUDA(cudaStreamSynchronize(s));
-    DARE_CUDA(cudaStreamSynchronize(cs));
-    tl_last_fallback = (int64_t)fb;
-    return;
-  }
   for (int32_t p0 = 0; p0 < n_poses; p0 += 65535) {
     int32_t np = std::min<int32_t>(65535, n_poses - p0);
     size_t off = (size_t)p0 * width * height;

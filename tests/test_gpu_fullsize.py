@@ -98,35 +98,3 @@ def test_cfg2_compound_matches_oracle_on_slab(cfg2):
     lin, _ = oracle.frame_cells(frames[0], wl.size, wl.size, sweep.pixel_pitch, s.origin, wl.voxel, s.dims)
     assert (lin >= 0).all()
     assert (np.asarray(s.flags)[lin] == 1).all()
-
-
-def test_cfg2_pinned_chunked_call_equals_single_launch(cfg2):
-    """dare_reslice into pinned host buffers with >= 32 poses launches pose
-    chunks whose device->host copies overlap the next chunk's kernels; the
-    bytes equal the single-launch path (pageable buffers) and the fallback
-    count is the batch's."""
-    import ctypes
-
-    import torch
-
-    from paper_2605_26325_b200 import _lib
-    from paper_2605_26325_b200.reslice import kernel_cfg, plane_params
-
-    wl, sweep, vol = cfg2
-    planes = bench_data.reslice_planes(wl, 48, seed=9)
-    cfg = db.ResliceConfig(interp_radius=wl.voxel)
-    px, cov, _ = db.reslice_batch(vol, planes, cfg)  # pageable: one launch
-    fb_single = ctypes.c_int64()
-    _lib.call("dare_reslice_last_fallback", ctypes.byref(fb_single))
-    params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
-    h, w = planes[0].height, planes[0].width
-    ppx = torch.empty((len(planes), h, w), dtype=torch.uint8).pin_memory().numpy()
-    pcov = torch.empty((len(planes), h, w), dtype=torch.uint8).pin_memory().numpy()
-    kc = kernel_cfg(cfg)
-    _lib.call("dare_reslice", vol.device_handle().raw, len(planes), _lib.ptr(params, ctypes.c_double), w, h,
-              ctypes.byref(kc), _lib.ptr(ppx, ctypes.c_uint8), _lib.ptr(pcov, ctypes.c_uint8))
-    fb = ctypes.c_int64()
-    _lib.call("dare_reslice_last_fallback", ctypes.byref(fb))
-    np.testing.assert_array_equal(ppx, px)
-    np.testing.assert_array_equal(pcov.view(bool), cov)
-    assert fb.value == fb_single.value
