@@ -258,6 +258,40 @@ def reconstruct_subset(sweep, frames: list[OracleFrame], origin, voxel, dims) ->
                 np.concatenate(ints))
 
 
+def cell_records(sweep, origin, voxel, dims, cells):
+    """Slab oracle: the exact sample list of each cell in
+    `cells`, in the reference's insertion order (synchronized frame order, then
+    row-major pixels; volume.py:240-256), streamed frame by frame through the
+    same frame_cells restatement -- no full volume is built.  Returns
+    {cell: (positions f32 (k,3), quaternions f32 (k,4), intensities u8 (k))}."""
+    images = sweep.images
+    _, h, w = images.shape
+    nc = int(np.prod(dims))
+    lut = np.zeros(nc, dtype=bool)
+    cells = np.asarray(cells, dtype=np.int64)
+    lut[cells] = True
+    parts = {int(c): ([], [], []) for c in cells}
+    for f in frame_poses(sweep):
+        lin, pos = frame_cells(f, w, h, sweep.pixel_pitch, origin, voxel, dims)
+        ok = lin >= 0
+        hit = np.zeros_like(ok)
+        hit[ok] = lut[lin[ok]]
+        if not hit.any():
+            continue
+        img = np.asarray(images[f.image]).reshape(-1)
+        q = _canon32(f.quat)
+        for i in np.nonzero(hit)[0]:  # row-major pixel order
+            p = parts[int(lin[i])]
+            p[0].append(pos[i])
+            p[1].append(q)
+            p[2].append(img[i])
+    out = {}
+    for c, (ps, qs, its) in parts.items():
+        out[c] = (np.array(ps, np.float32).reshape(-1, 3), np.array(qs, np.float32).reshape(-1, 4),
+                  np.array(its, np.uint8))
+    return out
+
+
 def seal_samples(origin, voxel, dims, positions, orientations, intensities) -> OracleVolume:
     """VolumeBuilder.insert_batch + seal (volume.py:223-269) for arbitrary samples."""
     pos = np.ascontiguousarray(positions, dtype=np.float32).reshape(-1, 3)

@@ -98,3 +98,50 @@ def test_cfg2_compound_matches_oracle_on_slab(cfg2):
     lin, _ = oracle.frame_cells(frames[0], wl.size, wl.size, sweep.pixel_pitch, s.origin, wl.voxel, s.dims)
     assert (lin >= 0).all()
     assert (np.asarray(s.flags)[lin] == 1).all()
+
+
+def test_cfg2_sampled_cells_records_match_slab_oracle(cfg2):
+    """SURVEY §8c (1) at BASELINE configs[1] scale: for 100k random cells the
+    exact sample list in the reference's insertion order (positions' bits,
+    canonical f32 quaternions, intensities) streamed from the frames by the
+    oracle, against the device volume read through perm."""
+    import bench
+    from cells_io import assert_cells_equal, device_cell_records
+
+    wl, sweep, vol = cfg2
+    host = bench.host_sweep(wl, sweep.images.cpu().numpy())
+    rng = np.random.default_rng(21)
+    cells = np.sort(rng.choice(int(np.prod(vol.dims)), 100_000, replace=False))
+    ref = oracle.cell_records(host, vol.origin, vol.voxel_size, vol.dims, cells)
+    n = assert_cells_equal(device_cell_records(vol, cells), ref)
+    assert n > 1_000_000
+
+
+def test_cfg2_certified_equals_exact_on_1024_poses(cfg2):
+    """The certified f32 path against the FP64-everywhere path on 1024 cfg2
+    poses (256^2): identical pixels and coverage (stress of the
+    error bound at the headline config)."""
+    import ctypes
+
+    from paper_2605_26325_b200 import _lib
+    from paper_2605_26325_b200.reslice import kernel_cfg, plane_params
+
+    wl, sweep, vol = cfg2
+    planes = bench_data.reslice_planes(wl, 1024, seed=77)
+    cfg = db.ResliceConfig(interp_radius=wl.voxel)
+    params = np.ascontiguousarray([plane_params(p) for p in planes], dtype=np.float64)
+    h = w = wl.plane
+    out = {}
+    fb = {}
+    for exact in (0, 1):
+        px = np.empty((len(planes), h, w), np.uint8)
+        cov = np.empty((len(planes), h, w), np.uint8)
+        kc = kernel_cfg(cfg, 0, exact=bool(exact))
+        _lib.call("dare_reslice", vol.device_handle().raw, len(planes), _lib.ptr(params, ctypes.c_double), w, h,
+                  ctypes.byref(kc), _lib.ptr(px, ctypes.c_uint8), _lib.ptr(cov, ctypes.c_uint8))
+        n = ctypes.c_int64()
+        _lib.call("dare_reslice_last_fallback", ctypes.byref(n))
+        out[exact], fb[exact] = (px, cov), n.value
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert fb[1] == 0 and 0 < fb[0] < 0.01 * len(planes) * h * w

@@ -97,3 +97,39 @@ def test_cfg4_trajectory_batch_equals_single_calls(cfg3):
         np.testing.assert_array_equal(px[k], one.pixels)
         np.testing.assert_array_equal(cov[k], one.coverage)
     assert cov.mean() > 0.5
+
+
+def test_cfg3_sampled_cells_records_match_slab_oracle(cfg3):
+    """SURVEY §8c (1) at BASELINE configs[2] scale (2.1 G samples, four sweeps):
+    100k random cells' exact insertion-order sample lists streamed from the
+    8000 frames by the oracle, against the device volume read through perm."""
+    import bench
+    from cells_io import assert_cells_equal, device_cell_records
+    from oracle import oracle
+
+    wl, sweep, vol = cfg3
+    host = bench.host_sweep(wl, sweep.images.cpu().numpy())
+    rng = np.random.default_rng(31)
+    cells = np.sort(rng.choice(int(np.prod(vol.dims)), 100_000, replace=False))
+    ref = oracle.cell_records(host, vol.origin, vol.voxel_size, vol.dims, cells)
+    n = assert_cells_equal(device_cell_records(vol, cells), ref)
+    assert n > 1_000_000
+
+
+def test_cfg4_trajectory_patches_match_slab_oracle(cfg3):
+    """cfg4 (haptic trajectory on the cfg3 volume): 64x64 centre patches of
+    trajectory planes from different base orientations against the slab
+    oracle, bit-exact."""
+    import bench
+
+    wl, sweep, vol = cfg3
+    host = bench.host_sweep(wl, sweep.images.cpu().numpy())
+    cfg = db.ResliceConfig(interp_radius=wl.voxel)
+    traj = bench_data.trajectory_planes(bench_data.workload("cfg4"), 7501, seed=4)
+    planes = [bench.patch_plane(traj[k], 64) for k in (300, 2900, 7500)]  # bases A, B, D
+    slab = bench.OracleSlab(wl, host)
+    px, cov, _ = db.reslice_batch(vol, planes, cfg)
+    for k, plane in enumerate(planes):
+        _, rp, rc, nf = slab.reslice(plane, cfg)
+        np.testing.assert_array_equal(px[k], rp)
+        np.testing.assert_array_equal(cov[k], rc)

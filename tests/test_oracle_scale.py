@@ -70,3 +70,20 @@ def test_bench_geometry_is_the_reference_sweep(name, cfg):
         np.testing.assert_array_equal([r.w, r.x, r.y, r.z], pq)
         np.testing.assert_array_equal(p.pose.translation, pt)
         assert p.pixel_pitch[0] == float(SCALE[f"{name}.plane_pitch"])
+
+
+def test_oracle_cell_records_equal_its_full_reconstruction():
+    """The streamed sampled-cell restatement used at cfg2/cfg3 scale
+    (oracle.cell_records) equals the full oracle volume's runs at cfg1 (itself
+    pinned to the reference's .darevol above)."""
+    frames = SCALE.frames("cfg1")
+    sweep = SCALE.sweep("cfg1", frames)
+    vol = oracle.reconstruct(sweep, 0.25, 0.0)
+    rng = np.random.default_rng(1)
+    cells = np.sort(rng.choice(int(np.prod(vol.dims)), 3000, replace=False))
+    ref = oracle.cell_records(sweep, vol.origin, vol.voxel_size, vol.dims, cells)
+    for c in cells:
+        a, b = vol.cell_starts[c], vol.cell_counts[c]
+        p, q, i = ref[int(c)]
+        assert np.array_equal(p, vol.positions[a:a + b]) and np.array_equal(q, vol.orientations[a:a + b])
+        assert np.array_equal(i, vol.intensities[a:a + b])
