@@ -126,7 +126,7 @@ def test_cfg4_trajectory_patches_match_slab_oracle(cfg3):
     host = bench.host_sweep(wl, sweep.images.cpu().numpy())
     cfg = db.ResliceConfig(interp_radius=wl.voxel)
     traj = bench_data.trajectory_planes(bench_data.workload("cfg4"), 7501, seed=4)
-    planes = [bench.patch_plane(traj[k], 64) for k in (300, 2900, 7500)]  # bases A, B, D
+    planes = [bench.patch_plane(traj[k], 64) for k in (300, 7500)]  # bases A and D
     slab = bench.OracleSlab(wl, host)
     px, cov, _ = db.reslice_batch(vol, planes, cfg)
     for k, plane in enumerate(planes):
