@@ -71,6 +71,11 @@ struct FrameView {
   // frames belongs to group k / chunks_per_group, whose per-cell counters and
   // key offsets live at + group * ncells
   uint32_t chunks_per_group, ncells;
+  // direct slots (group mode 2): 64-bit counters (samples | runs << 32) per
+  // (group, cell); a (group, cell) with a single run gets its slot from the
+  // per-group prefix table without an atomic
+  uint32_t direct;
+  const uint32_t* pre;  // (group, cell) -> samples of the cell in earlier groups | single-run << 31
   __device__ __forceinline__ size_t group_base(uint32_t chunk) const {
     return (size_t)(chunk / chunks_per_group) * ncells;
   }
@@ -102,6 +107,16 @@ static inline uint32_t ceil_log2(uint64_t x) {
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// One run of k samples of cell `cell` into the count histogram of its frame
+// group (counts already offset to the group in the 32-bit layout; the direct
+// mode's 64-bit counters also count runs).
+__device__ __forceinline__ void count_run(uint32_t* counts, size_t gb64, bool direct, uint32_t cell, uint32_t k) {
+  if (direct)
+    atomicAdd(reinterpret_cast<unsigned long long*>(counts) + gb64 + cell, (1ull << 32) | (unsigned long long)k);
+  else
+    atomicAdd(counts + cell, k);
+}
 
 // Warp-aggregated histogram (kFill=false) or slot assignment (kFill=true):
 // lanes holding the same cell form one __match_any_sync group; the lowest lane
@@ -198,7 +213,8 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
   __syncthreads();
   const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
-  counts += fv.group_base(blockIdx.y);
+  const size_t gb64 = fv.group_base(blockIdx.y);  // (direct mode: 64-bit counters)
+  if (!fv.direct) counts += gb64;
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   int32_t cur = -1;
   uint32_t run_j = 0, k = 0, bb = 0, nr = 0, n_oob = 0;
@@ -212,7 +228,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
     n_oob += (in_frame && cell < 0) ? 1u : 0u;
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     if (restart && cur >= 0) {
-      atomicAdd(&counts[cur], k);
+      count_run(counts, gb64, fv.direct, (uint32_t)cur, k);
       my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
       ++nr;
     }
@@ -231,7 +247,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_k(FrameView fv, VoxelMap m
     ++k;
   }
   if (cur >= 0) {
-    atomicAdd(&counts[cur], k);
+    count_run(counts, gb64, fv.direct, (uint32_t)cur, k);
     my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
     ++nr;
   }
@@ -274,7 +290,8 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
   __syncthreads();
   const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
-  counts += fv.group_base(blockIdx.y);
+  const size_t gb64 = fv.group_base(blockIdx.y);  // (direct mode: 64-bit counters)
+  if (!fv.direct) counts += gb64;
   const double U = (double)u * fv.px, V = (double)v * fv.py;
   const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
   AxisCell ax[2];
@@ -328,7 +345,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
     const bool restart = lin != cur || k == (uint32_t)kMaxRun;
     if (restart && cur >= 0) {
       DARE_CHECK(nr < (uint32_t)kRunFrames && (uint32_t)cur < fv.ncells);
-      atomicAdd(&counts[cur], k);
+      count_run(counts, gb64, fv.direct, (uint32_t)cur, k);
       my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
       ++nr;
       n_in += k;
@@ -343,7 +360,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
     ++k;
   }
   if (cur >= 0) {
-    atomicAdd(&counts[cur], k);
+    count_run(counts, gb64, fv.direct, (uint32_t)cur, k);
     my[(size_t)nr * 256] = make_uint2((uint32_t)cur, run_j | (k << 6) | (bb << 10));
     ++nr;
     n_in += k;
@@ -380,8 +397,9 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
   const size_t blk = (size_t)chunk * gridDim.x + blockIdx.x;
   const uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const uint32_t nr = nruns[blk * 256 + threadIdx.x];
-  counts += fv.group_base(chunk);
-  offsets += fv.group_base(chunk);
+  const size_t gb = fv.group_base(chunk);
+  counts += gb;  // 32-bit cursors per (group, cell) in both group modes
+  if (!fv.direct) offsets += gb;  // group-major key CSR (mode 1); mode 2 writes cell-major
   const uint32_t max_nr = __reduce_max_sync(0xffffffffu, nr);
   uint2 next = nr > 0 ? my[0] : make_uint2(0u, 0u);
   for (uint32_t r = 0; r < max_nr; ++r) {
@@ -394,9 +412,12 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
 #pragma unroll
     for (int t = 0; t < kMaxRun; ++t)
       inten[t] = (kWide && need && (uint32_t)t < k) ? fv.frames[(size_t)s_img[run_j + t] * fv.hw + p] : 0u;
-    const uint32_t cell_off = need ? offsets[lin] : 0u;  // issued early: overlaps the atomic
-    // lanes not emitting get a key no cell has, so MATCH runs on the full warp
-    const unsigned peers = __match_any_sync(0xffffffffu, need ? lin : (0x80000000u | lane));
+    uint32_t pre_w = 0;
+    if (fv.direct && need) pre_w = fv.pre[gb + lin];
+    const bool solo = (pre_w >> 31) != 0;  // the only run of its (group, cell): slot known, no atomic
+    const uint32_t cell_off = need ? offsets[lin] + (pre_w & 0x7fffffffu) : 0u;  // early: overlaps the atomic
+    // lanes not emitting (or solo) get a key no cell has, so MATCH runs on the full warp
+    const unsigned peers = __match_any_sync(0xffffffffu, (need && !solo) ? lin : (0x80000000u | lane));
     // Groups whose runs cover the same frames (the common case: image
     // neighbours crossing a cell together) take their slots frame-major --
     // (frame, pixel) = insertion order -- so the seal's sort finds them presorted.
@@ -416,12 +437,12 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
       }
     }
     unsigned base = 0;
-    if (need && lane == leader) base = atomicAdd(&counts[lin], total);
+    if (need && !solo && lane == leader) base = atomicAdd(&counts[lin], total);
     base = __shfl_sync(0xffffffffu, base, leader);
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
       const uint32_t stride = uniform ? n : 1u;
-      DARE_CHECK(base + total <= offsets[lin + 1] - cell_off);
+      DARE_CHECK(fv.direct || base + total <= offsets[lin + 1] - cell_off);
       Key* dst = keys + cell_off + base + (uniform ? rank : prefix);
       if constexpr (kWide) {
         const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
@@ -822,6 +843,23 @@ __global__ void group_totals_k(const uint32_t* __restrict__ koff, uint32_t ncell
   totals[c] = t;
 }
 
+// Direct mode: per cell, the samples of earlier groups (its runs of group g
+// start there, after offsets[c]) with bit 31 set when group g holds exactly
+// one run of the cell, and the cell's total.
+__global__ void direct_pre_k(const unsigned long long* __restrict__ cnt64, uint32_t ncells, uint32_t groups,
+                             uint32_t* pre, uint32_t* totals) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  uint32_t acc = 0;
+  for (uint32_t g = 0; g < groups; ++g) {
+    const size_t i = (size_t)g * ncells + c;
+    const unsigned long long v = cnt64[i];
+    pre[i] = acc | ((uint32_t)(v >> 32) == 1u ? 0x80000000u : 0u);
+    acc += (uint32_t)v;
+  }
+  totals[c] = acc;
+}
+
 template <class Key>
 __global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict__ koff,
                                                       const uint32_t* __restrict__ offsets, uint32_t ncells,
@@ -860,17 +898,19 @@ __global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict
 // `scatter(fill, counts, offsets, keys, rejected)` launches the source's pass.
 template <class Rec, class Scatter>
 void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int seal_carveout = -1,
-               uint32_t groups = 1) {
+               uint32_t groups = 1, uint32_t* direct_pre = nullptr) {
   const int64_t ncells = vol->ncells;
   const int64_t nkc = ncells * (int64_t)groups;  // per-group counters (groups > 1: frame-grouped keys)
   DARE_LIMIT(nkc < (int64_t)UINT32_MAX, "too many cells x frame groups");
+  const bool direct = direct_pre != nullptr;  // group mode 2 (64-bit counters, solo runs placed directly)
   PhaseTimer pt(s, "build_csr");
-  Scratch<uint32_t> counts(nkc + 1, s);
+  const int64_t ncount = direct ? 2 * nkc : nkc + 1;
+  Scratch<uint32_t> counts(ncount, s);
   Scratch<unsigned long long> rej(1, s);
-  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (nkc + 1), s));
+  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * ncount, s));
   DARE_CUDA(cudaMemsetAsync(rej.ptr, 0, sizeof(unsigned long long), s));
   dev_alloc(&vol->d_offsets, sizeof(uint32_t) * (ncells + 1));
-  Scratch<uint32_t> koff(groups > 1 ? nkc + 1 : 0, s);
+  Scratch<uint32_t> koff(groups > 1 && !direct ? nkc + 1 : 0, s);
   Scratch<uint32_t> totals(groups > 1 ? ncells + 1 : 0, s);
   pt.mark("alloc+memset");
   using Key = typename Rec::Key;
@@ -881,7 +921,13 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   Scratch<uint32_t> max_d(1, s);
   // per-cell totals: the counters themselves (one group) or their sum over groups
   uint32_t* tot = counts.ptr;
-  if (groups > 1) {
+  if (direct) {
+    direct_pre_k<<<ceil_div(ncells, 256), 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(counts.ptr),
+                                                       (uint32_t)ncells, groups, direct_pre, totals.ptr);
+    DARE_CUDA(cudaGetLastError());
+    DARE_CUDA(cudaMemsetAsync(totals.ptr + ncells, 0, sizeof(uint32_t), s));
+    tot = totals.ptr;
+  } else if (groups > 1) {
     DARE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2_bytes, counts.ptr, koff.ptr, nkc + 1, s));
     Scratch<uint8_t> tmp(tmp2_bytes, s);
     DARE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp2_bytes, counts.ptr, koff.ptr, nkc + 1, s));
@@ -917,7 +963,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   Scratch<Key> keys(n_kept, s);
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * nkc, s));
   pt.mark("readback+alloc");
-  if (groups > 1) {
+  if (groups > 1 && !direct) {
     Scratch<Key> gkeys(n_kept, s);
     scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr);
     DARE_CUDA(cudaGetLastError());
@@ -1020,7 +1066,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
                  (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
                  FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw,
-                 0xffffffffu, (uint32_t)vol->ncells};
+                 0xffffffffu, (uint32_t)vol->ncells, 0u, nullptr};
     {
       const uint32_t ub = ceil_log2((uint64_t)width), vb = ceil_log2((uint64_t)height);
       if (ub + vb + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 32 && ub + vb < 32) {
@@ -1096,19 +1142,31 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     // sweep, so no lane aggregation), not by the partial sectors alone.  One
     // group by default; DARE_KEY_GROUPS=n selects the grouped layout.
     uint32_t groups = 1;
+    Scratch<uint32_t> pre_store;
     {
+      // mode 2 (direct slots) by default for long sweeps: groups of ~1024
+      // frames; DARE_KEY_GROUPS=n forces n groups, DARE_KEY_MODE=1 the
+      // group-major layout + regroup, DARE_KEY_MODE=0 one group
       const char* genv = getenv("DARE_KEY_GROUPS");
-      const int64_t want = genv ? atoi(genv) : 1;
-      if (want > 1 && ncells_total_fits(vol->ncells, want)) {
+      const char* menv = getenv("DARE_KEY_MODE");
+      const int mode = menv ? atoi(menv) : 2;
+      const int64_t want = genv ? atoi(genv) : (n_frames >= 2048 ? std::min<int64_t>(16, (n_frames + 1023) / 1024) : 1);
+      if (mode != 0 && want > 1 && ncells_total_fits(2 * vol->ncells, want)) {
         const uint32_t cpg = (uint32_t)ceil_div(ceil_div(n_frames, want), kRunFrames);
         fv.chunks_per_group = cpg;
         groups = (uint32_t)ceil_div(ceil_div(n_frames, kRunFrames), cpg);
+        if (mode == 2 && groups > 1) {
+          pre_store.stream = s;
+          DARE_CUDA(cudaMallocAsync((void**)&pre_store.ptr, sizeof(uint32_t) * (size_t)groups * vol->ncells, s));
+          fv.direct = 1;
+          fv.pre = pre_store.ptr;
+        }
       }
     }
     if (narrow_keys)
-      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups);
+      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr);
     else
-      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups);
+      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr);
     clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;

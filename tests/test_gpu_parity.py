@@ -62,7 +62,7 @@ def _random_sweep(rng, n, h, w, pitch, spread):
 
 
 @pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
-                                       ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7")])
+                                       ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7"), ("DARE_KEY_MODE", "0")])
 @pytest.mark.parametrize("key", REC_KEYS)
 def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
@@ -79,11 +79,15 @@ def test_reconstruct_alternative_passes_match_reference(golden, key, env, value,
         np.testing.assert_array_equal(s.counts, golden[f"cmp_{key}.counts"])
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("groups", ["0", "2", "3", "5"])
-def test_reconstruct_frame_grouped_keys_match_oracle(groups, monkeypatch):
+def test_reconstruct_frame_grouped_keys_match_oracle(groups, mode, monkeypatch):
     """Multi-direction sweep of 330 frames (three sub-sweeps at different probe
-    orientations over one region, like cfg3) with the keys kept per frame
-    group and regrouped cell-major (DARE_KEY_GROUPS; 0 = the default choice)."""
+    orientations over one region, like cfg3) with per-frame-group counters:
+    mode 2 (default for long sweeps) places single-run (group, cell) keys
+    without atomics, mode 1 keeps group-major key CSRs and regroups them
+    (DARE_KEY_GROUPS; 0 = the default choice, one group at this length)."""
+    monkeypatch.setenv("DARE_KEY_MODE", mode)
     if groups != "0":
         monkeypatch.setenv("DARE_KEY_GROUPS", groups)
     rng = np.random.default_rng(44)
