@@ -1144,13 +1144,16 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     uint32_t groups = 1;
     Scratch<uint32_t> pre_store;
     {
-      // mode 2 (direct slots) by default for long sweeps: groups of ~1024
-      // frames; DARE_KEY_GROUPS=n forces n groups, DARE_KEY_MODE=1 the
-      // group-major layout + regroup, DARE_KEY_MODE=0 one group
+      // Opt-in (measured at cfg3, profiles/round2_recon_variants.md): mode 2
+      // (direct slots) fill 35.5 ms vs 35-38 ms with one group -- the cfg3
+      // fill is not bound by its returning atomics either; mode 1 (group-major
+      // key CSRs + regroup) removes the partial-sector DRAM merges (fill 26 ms)
+      // but its regroup and counters cost more.  DARE_KEY_GROUPS=n selects n
+      // groups of frames, DARE_KEY_MODE the layout (2 when groups are requested).
       const char* genv = getenv("DARE_KEY_GROUPS");
       const char* menv = getenv("DARE_KEY_MODE");
       const int mode = menv ? atoi(menv) : 2;
-      const int64_t want = genv ? atoi(genv) : (n_frames >= 2048 ? std::min<int64_t>(16, (n_frames + 1023) / 1024) : 1);
+      const int64_t want = genv ? atoi(genv) : 1;
       if (mode != 0 && want > 1 && ncells_total_fits(2 * vol->ncells, want)) {
         const uint32_t cpg = (uint32_t)ceil_div(ceil_div(n_frames, want), kRunFrames);
         fv.chunks_per_group = cpg;
