@@ -27,7 +27,7 @@ for f in ("ev_pytest_gpu.log", "ev_smoke.log"):
     if os.path.exists(os.path.join(G, f)):
         shutil.copy(os.path.join(G, f), os.path.join(P, f"{TAG}_{f[3:]}"))
 shutil.copy(os.path.join(G, "ev_launches_cfg2.csv"), os.path.join(P, f"{TAG}_launches_cfg2.csv"))
-reps = {t: os.path.join(G, f"ev_prof_{t}.ncu-rep") for t in
+reps = {t: os.path.join(G, f"ev_raw_{t}.csv") for t in
         ("reslice", "fallback", "prep", "count", "fill", "seal", "compound", "fillpass", "trilinear")}
 reps = {t: r for t, r in reps.items() if os.path.exists(r)}
 tr = {}
