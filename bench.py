@@ -66,8 +66,11 @@ def parse_args():
 # ----------------------------------------------------------------------------- helpers
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    polled every 2 ms from a thread (a cfg2 timed region is ~40 ms), with
+    nvidia-smi -lms 50 as the fallback when NVML is unavailable."""
 
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -76,8 +79,24 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self.nvml = None
+        self._stop = threading.Event()
+        self._thread = None
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self._thread = threading.Thread(target=self._poll, daemon=True)
+            self._thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -86,11 +105,34 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        p = self.nvml
+        while not self._stop.is_set():
+            try:
+                sm = float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+                reasons = int(p.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                self.samples.append((sm, self.smax, reasons))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
+        if self.nvml is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
+            p = self.nvml
+            bits = {"hw_slowdown": p.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": p.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": p.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": p.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({n for _, _, r in self.samples for n, b in bits.items() if r & b})
+            sm = [x for x, _, _ in self.samples]
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax, "reasons": reasons,
+                    "samples": len(sm), "source": "nvml, 2 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         time.sleep(0.06)
@@ -100,7 +142,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 8:
@@ -110,11 +151,11 @@ class ClockSampler:
                 smax.append(float(parts[1]))
             except ValueError:
                 continue
-            for name, flag in zip(names, parts[4:8]):
+            for name, flag in zip(self.NAMES, parts[4:8]):
                 if flag.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi, 50 ms"}
 
 
 class DevArray:
@@ -169,7 +210,9 @@ def _pow2(x: float) -> bool:
 def ncu_traffic(kernel: str, batch: int, config: str):
     """DRAM bytes (read+write) per launch of `kernel` from the committed ncu capture
     (profiles/round1_traffic.json, cfg2 with 64 poses per launch), or None."""
-    path = os.path.join(ROOT, "profiles", "round1_traffic.json")
+    path = os.path.join(ROOT, "profiles", "round2_traffic.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "round1_traffic.json")
     try:
         with open(path) as fh:
             data = json.load(fh)
@@ -179,7 +222,7 @@ def ncu_traffic(kernel: str, batch: int, config: str):
         # (captures before the parts-per-pixel template argument printed it as the bool 0)
         alt = kernel[:-2] + "0>" if kernel.endswith(", 1>") else kernel
         key = kernel if kernel in table else alt
-        return float(table[key]), "profiles/round1_traffic.json (" + data["source"] + ")"
+        return float(table[key]), f"profiles/{os.path.basename(path)} (" + data["source"] + ")"
     except Exception as e:  # noqa: BLE001
         return None, f"no ncu capture ({type(e).__name__})"
 

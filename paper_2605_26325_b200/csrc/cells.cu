@@ -124,52 +124,62 @@ bool build_cell_tables_host(const VoxelMap& m, bool zfine, std::vector<double>& 
 
 bool build_cell_tables(const VoxelMap& m, bool zfine, cudaStream_t s, Scratch<double>& storage,
                        CellTables& out) {
-  // small per-process cache: rebuilding a volume on the same grid reuses the tables
+  // per-process cache of the tables, on the device as well: rebuilding a
+  // volume (or compounding) on the same grid costs no host work and no
+  // upload.  Entries are never freed (kernels of other threads may use them);
+  // past kMaxEntries grids the tables go into the caller's scratch instead.
+  constexpr size_t kMaxEntries = 64;
   struct Entry {
+    int device;
     double key[8];
-    std::vector<double> host;
-    size_t off[3];
-    int n[3];
     bool ok;
+    int n[3];
+    size_t off[3];
+    double* d;  // device copy
   };
   static std::mutex mu;
-  static std::vector<Entry> cache;  // most recent last, <= 8 entries
+  static std::vector<Entry> cache;
+  int dev = 0;
+  DARE_CUDA(cudaGetDevice(&dev));
   const double key[8] = {m.origin[0], m.origin[1], m.origin[2], m.voxel, (double)m.dims[0], (double)m.dims[1],
                          (double)m.dims[2], zfine ? 1.0 : 0.0};
-  std::vector<double> host;
-  size_t off[3];
-  bool ok = false, hit = false;
   {
     std::lock_guard<std::mutex> lock(mu);
     for (const Entry& e : cache)
-      if (std::memcmp(e.key, key, sizeof(key)) == 0) {
-        host = e.host;
-        std::memcpy(off, e.off, sizeof(off));
+      if (e.device == dev && std::memcmp(e.key, key, sizeof(key)) == 0) {
+        if (!e.ok) return false;
         std::memcpy(out.n, e.n, sizeof(e.n));
-        ok = e.ok;
-        hit = true;
-        break;
+        for (int a = 0; a < 3; ++a) out.t[a] = e.d + e.off[a];
+        out.zfine = zfine ? 1 : 0;
+        return true;
       }
   }
-  if (!hit) {
-    ok = build_cell_tables_host(m, zfine, host, off, out.n);
-    std::lock_guard<std::mutex> lock(mu);
-    Entry e;
-    std::memcpy(e.key, key, sizeof(key));
-    e.host = host;
-    std::memcpy(e.off, off, sizeof(off));
-    std::memcpy(e.n, out.n, sizeof(e.n));
-    e.ok = ok;
-    if (cache.size() >= 8) cache.erase(cache.begin());
-    cache.push_back(std::move(e));
+  std::vector<double> host;
+  Entry e;
+  e.device = dev;
+  std::memcpy(e.key, key, sizeof(key));
+  e.ok = build_cell_tables_host(m, zfine, host, e.off, e.n);
+  e.d = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (e.ok && cache.size() < kMaxEntries) {
+    DARE_CUDA(cudaMalloc((void**)&e.d, sizeof(double) * host.size()));
+    DARE_CUDA(cudaMemcpy(e.d, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+    cache.push_back(e);
+  } else if (!e.ok && cache.size() < kMaxEntries) {
+    cache.push_back(e);
   }
-  if (!ok) return false;
+  if (!e.ok) return false;
+  std::memcpy(out.n, e.n, sizeof(e.n));
   out.zfine = zfine ? 1 : 0;
-  // storage is an empty Scratch owned by the caller (freed on its scope exit)
+  if (e.d) {
+    for (int a = 0; a < 3; ++a) out.t[a] = e.d + e.off[a];
+    return true;
+  }
+  // cache full: the caller's stream-ordered scratch
   DARE_CUDA(cudaMallocAsync((void**)&storage.ptr, sizeof(double) * host.size(), s));
   storage.stream = s;
   DARE_CUDA(cudaMemcpyAsync(storage.ptr, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, s));
-  for (int a = 0; a < 3; ++a) out.t[a] = storage.ptr + off[a];
+  for (int a = 0; a < 3; ++a) out.t[a] = storage.ptr + e.off[a];
   return true;
 }
 

@@ -17,6 +17,7 @@
 //  trilinear : thread per pixel, 8 corners in (cx, cy, cz) order, f32 values
 //              read directly (the reference's per-call f64 copy of the whole
 //              grid, baseline.py:142-149, is pure overhead: f32->f64 is exact).
+#include <cmath>
 #include <memory>
 #include <vector>
 
@@ -104,6 +105,10 @@ __global__ void __launch_bounds__(256) compound_k(ScalarFrameView fv, VoxelMap m
 // per frame two compares per axis against the current cell's interval, the
 // f64 in-plane product reused across frames with identical axis columns,
 // 32-bit cells and a 32-bit MATCH for the warp-aggregated flush.
+// kPacked: one 64-bit atomic per flush into count << 40 | sum (the host
+// enables it only when no cell can collect 2^24 observations, so the sum,
+// <= 255 * count, stays below 2^40); split into sums / counts afterwards.
+template <bool kPacked>
 __device__ __forceinline__ void compound_flush32(bool need, int32_t lin, unsigned sum, unsigned cnt,
                                                  unsigned long long* sums, unsigned long long* counts) {
   const unsigned lane = threadIdx.x & 31u;
@@ -112,11 +117,27 @@ __device__ __forceinline__ void compound_flush32(bool need, int32_t lin, unsigne
   const unsigned total = __reduce_add_sync(peers, sum);
   const unsigned n = __reduce_add_sync(peers, cnt);
   if (need && lane == (unsigned)(__ffs(peers) - 1)) {
-    atomicAdd(&sums[lin], (unsigned long long)total);
-    atomicAdd(&counts[lin], (unsigned long long)n);
+    if (kPacked) {
+      atomicAdd(&sums[lin], ((unsigned long long)n << 40) | (unsigned long long)total);
+    } else {
+      atomicAdd(&sums[lin], (unsigned long long)total);
+      atomicAdd(&counts[lin], (unsigned long long)n);
+    }
   }
 }
 
+// packed -> the caller's (accumulating) sums / counts
+__global__ void compound_unpack_k(int64_t n, const unsigned long long* __restrict__ packed,
+                                  unsigned long long* sums, unsigned long long* counts) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const unsigned long long v = packed[c];
+  if (v == 0) return;
+  sums[c] += v & ((1ull << 40) - 1);
+  counts[c] += v >> 40;
+}
+
+template <bool kPacked>
 __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTables ct, VoxelMap m,
                                                       unsigned long long* sums, unsigned long long* counts) {
   __shared__ double s_axes[kCFrames * 9];
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTa
     const unsigned inten = in_frame ? (unsigned)fv.frames[s_img[j] + p] : 0u;
     const bool change = lin != cur;
     const bool need = change && cur >= 0;
-    if (__any_sync(0xffffffffu, need)) compound_flush32(need, cur, sum, cnt, sums, counts);
+    if (__any_sync(0xffffffffu, need)) compound_flush32<kPacked>(need, cur, sum, cnt, sums, counts);
     if (change) {
       cur = lin;
       sum = 0;
@@ -189,7 +210,7 @@ __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTa
     sum += inten;
     cnt += 1;
   }
-  if (__any_sync(0xffffffffu, cur >= 0)) compound_flush32(cur >= 0, cur, sum, cnt, sums, counts);
+  if (__any_sync(0xffffffffu, cur >= 0)) compound_flush32<kPacked>(cur >= 0, cur, sum, cnt, sums, counts);
 }
 
 __global__ void compound_finalize_k(int64_t n, const unsigned long long* __restrict__ sums,
@@ -462,10 +483,30 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
       Scratch<double> tab_store;
       CellTables ct;
       const char* legacy = getenv("DARE_COUNT_LEGACY");
-      if (!(legacy && legacy[0] == '1') && m.dims[0] * m.dims[1] * m.dims[2] < (int64_t)INT32_MAX &&
-          build_cell_tables(m, false, s, tab_store, ct))
-        compound_tab_k<<<grid, 256, 0, s>>>(fv, ct, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
-      else
+      const int64_t ncells = m.dims[0] * m.dims[1] * m.dims[2];
+      if (!(legacy && legacy[0] == '1') && ncells < (int64_t)INT32_MAX &&
+          build_cell_tables(m, false, s, tab_store, ct)) {
+        // packed 64-bit flushes when lanes rarely share a cell (under 2 pixels per
+        // cell and frame: every flush is its own atomic pair) and no cell can
+        // reach 2^24 observations (a cell spans <= floor(sqrt3 v / p) + 2
+        // pixels per image axis, per frame)
+        const double per_frame = (std::floor(1.7320508075688772 * voxel_size / pitch_x) + 2.0) *
+                                 (std::floor(1.7320508075688772 * voxel_size / pitch_y) + 2.0);
+        const char* penv = getenv("DARE_COMPOUND_PACKED");  // development override (0 / 1)
+        const bool packed = penv ? penv[0] == '1'
+                                 : (voxel_size / pitch_x) * (voxel_size / pitch_y) < 2.0 &&
+                                       (double)n_frames * per_frame < 16777216.0;
+        if (packed && (double)n_frames * per_frame < 16777216.0) {
+          Scratch<unsigned long long> pk(ncells, s);
+          DARE_CUDA(cudaMemsetAsync(pk.ptr, 0, sizeof(unsigned long long) * ncells, s));
+          compound_tab_k<true><<<grid, 256, 0, s>>>(fv, ct, m, pk.ptr, nullptr);
+          compound_unpack_k<<<ceil_div(ncells, 256), 256, 0, s>>>(ncells, pk.ptr, (unsigned long long*)d_sums,
+                                                                  (unsigned long long*)d_counts);
+        } else {
+          compound_tab_k<false><<<grid, 256, 0, s>>>(fv, ct, m, (unsigned long long*)d_sums,
+                                                     (unsigned long long*)d_counts);
+        }
+      } else
         (m.exact_inv ? compound_k<true> : compound_k<false>)<<<grid, 256, 0, s>>>(
             fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
       pt.mark("compound_k");
