@@ -402,57 +402,57 @@ def _best_ms(fn, reps=3):
 def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
     """Config 5 (direction-blind comparison arm) on the same sweep: compound of
     the full sweep, fill_holes + trilinear on a sparse variant (every 8th frame,
-    SURVEY §8d) so that gap filling does real work.  Wall time of each C-ABI
-    call (frames in HBM); algorithmic bytes per SURVEY §8d."""
+    SURVEY §8d) so that gap filling does real work.  Per call: the wall time of
+    the public function (frames in HBM) and its device span (CUDA events on the
+    library stream, dare_last_device_ms); best of 4 after a warm-up call (the
+    first call of a size also grows the device pool).  Algorithmic bytes per
+    SURVEY §8d."""
     from types import SimpleNamespace
 
-    from paper_2605_26325_b200 import parallel
-    from paper_2605_26325_b200.sweep import plan_frames
+    def timed(fn, reps=4):
+        out = fn()  # warm-up
+        walls, devs = [], []
+        for _ in range(reps):
+            del out
+            t0 = time.perf_counter()
+            out = fn()
+            walls.append((time.perf_counter() - t0) * 1000.0)
+            devs.append(last_device_ms())
+        return min(walls), min(devs), out
 
     n_in = wl.n_frames * wl.size * wl.size
-    ms_c, sv = _best_ms(lambda: db.compound(dev_sweep, voxel_size=wl.voxel, margin=0.0))
+    ms_c, dev_c, sv = timed(lambda: db.compound(dev_sweep, voxel_size=wl.voxel, margin=0.0))
     ncells = int(np.prod(sv.dims))
-    # device time of the accumulate kernel (+ zeroing the u64 sums/counts), CUDA events
-    plan = plan_frames(dev_sweep)
-    st = torch.cuda.Stream()
-    dev_c = []
-    with torch.cuda.stream(st):
-        for _ in range(4):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            acc = parallel.CudaOps.compound_partial(dev_sweep, plan, 0, plan.n_frames, sv.origin, sv.voxel_size,
-                                                    sv.dims, stream=st.cuda_stream)
-            e1.record(st)
-            st.synchronize()
-            dev_c.append(e0.elapsed_time(e1))
-            del acc
-    dev_ms_c = min(dev_c[1:])
     sparse = SimpleNamespace(images=frames_d[::8].contiguous(), image_timestamps=dev_sweep.image_timestamps[::8],
                              pose_timestamps=dev_sweep.pose_timestamps[::8], poses=dev_sweep.poses[::8],
                              pixel_pitch=dev_sweep.pixel_pitch, calibration=dev_sweep.calibration, mask=None)
     sv_sparse = db.compound(sparse, voxel_size=wl.voxel, margin=0.0)
-    ms_f, filled = _best_ms(lambda: db.fill_holes(sv_sparse, 3))
+    ms_f, dev_f, filled = timed(lambda: db.fill_holes(sv_sparse, 3))
     passes = filled.passes_run
     nc_sparse = int(np.prod(sv_sparse.dims))
     db.reslice_trilinear_batch(filled, planes)
-    ms_t, _ = _best_ms(lambda: db.reslice_trilinear_batch(filled, planes))
+    walls = []
+    for _ in range(4):
+        t0 = time.perf_counter()
+        db.reslice_trilinear_batch(filled, planes)
+        walls.append((time.perf_counter() - t0) * 1000.0)
+    ms_t = min(walls)
     hw = planes[0].width * planes[0].height
-    tri_bytes = len(planes) * (8 * hw * 5 + hw * (1 + 1 / 8))  # <= 8 distinct corners per pixel
     comp_bytes = n_in + ncells * 5
     fill_bytes = passes * nc_sparse * 10
     gbs = lambda b, ms: b / (ms / 1000.0) / 1e9  # noqa: E731
     return {
-        "compound": {"ms": ms_c, "input_Mpix_per_s": n_in / 1e6 / (ms_c / 1000.0),
-                     "device_ms": dev_ms_c, "device_input_Mpix_per_s": n_in / 1e6 / (dev_ms_c / 1000.0),
-                     "algorithmic_GBps": gbs(comp_bytes, dev_ms_c), "frac": gbs(comp_bytes, dev_ms_c) / peak,
-                     "note": "ms = wall time of compound() (host plan + C-ABI call); device_ms = CUDA events "
-                             "around dare_compound_accumulate (zeroing + compound_k); frac uses device_ms"},
-        "fill_holes": {"ms": ms_f, "passes_run": passes, "cells": nc_sparse,
-                       "algorithmic_GBps": gbs(fill_bytes, ms_f) if passes else None,
+        "compound": {"ms": ms_c, "device_ms": dev_c, "input_Mpix_per_s": n_in / 1e6 / (ms_c / 1000.0),
+                     "device_input_Mpix_per_s": n_in / 1e6 / (dev_c / 1000.0),
+                     "algorithmic_GBps": gbs(comp_bytes, dev_c), "frac": gbs(comp_bytes, dev_c) / peak,
+                     "note": "ms = wall time of compound() (host plan + C-ABI call); device_ms = its device span "
+                             "(zeroing + compound_tab_k + finalize); frac uses device_ms"},
+        "fill_holes": {"ms": ms_f, "device_ms": dev_f, "passes_run": passes, "cells": nc_sparse,
+                       "algorithmic_GBps": gbs(fill_bytes, dev_f) if passes else None,
                        "sweep": f"every 8th frame ({len(sparse.poses)} frames)"},
         "trilinear": {"ms_per_batch": ms_t, "poses": len(planes), "reslices_per_s": len(planes) / (ms_t / 1000.0),
                       "note": "host-buffer C-ABI call incl. pose upload and image download"},
-        "timing": "best of 3 wall-clock C-ABI calls (each synchronises)",
+        "timing": "best of 4 calls after a warm-up call (each synchronises)",
     }
 
 
