@@ -482,9 +482,13 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
       dim3 grid(ceil_div(width, 16) * ceil_div(height, 16), ceil_div(n_frames, kCFrames));
       Scratch<double> tab_store;
       CellTables ct;
-      const char* legacy = getenv("DARE_COUNT_LEGACY");
+      // The threshold-table variant (compound_tab_k) measured slower than the
+      // FP64-chain kernel here (cfg2: 1.56 vs 1.09 ms; the per-crossing table
+      // walk's dependent loads sit on the flush path), unlike the count pass:
+      // opt-in with DARE_COMPOUND_TABLES=1.
+      const char* tabs = getenv("DARE_COMPOUND_TABLES");
       const int64_t ncells = m.dims[0] * m.dims[1] * m.dims[2];
-      if (!(legacy && legacy[0] == '1') && ncells < (int64_t)INT32_MAX &&
+      if ((tabs && tabs[0] == '1') && ncells < (int64_t)INT32_MAX &&
           build_cell_tables(m, false, s, tab_store, ct)) {
         // packed 64-bit flushes when lanes rarely share a cell (under 2 pixels per
         // cell and frame: every flush is its own atomic pair) and no cell can

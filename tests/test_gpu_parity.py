@@ -63,7 +63,7 @@ def _random_sweep(rng, n, h, w, pitch, spread):
 
 @pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
                                        ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7"), ("DARE_KEY_MODE", "0"),
-                                       ("DARE_COMPOUND_PACKED", "1"), ("DARE_COMPOUND_PACKED", "0")])
+                                       ("DARE_COMPOUND_TABLES", "1")])
 @pytest.mark.parametrize("key", REC_KEYS)
 def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
@@ -71,6 +71,8 @@ def test_reconstruct_alternative_passes_match_reference(golden, key, env, value,
     keys with the regroup pass -- the default for sweeps over ~1000 frames)
     give the same bytes as the default path."""
     monkeypatch.setenv(env, value)
+    if env == "DARE_COMPOUND_TABLES":
+        monkeypatch.setenv("DARE_COMPOUND_PACKED", "1" if key in ("rec_tilt", "rec_margin0") else "0")
     rec, voxel, margin = golden.sweep(key)
     v = db.reconstruct_volume(rec, voxel_size=voxel, margin=margin)
     assert_volume_equal(v, golden.volume(key + ".out"))
