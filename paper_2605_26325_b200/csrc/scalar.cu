@@ -213,6 +213,74 @@ __global__ void __launch_bounds__(256) compound_tab_k(ScalarFrameView fv, CellTa
   if (__any_sync(0xffffffffu, cur >= 0)) compound_flush32<kPacked>(cur >= 0, cur, sum, cnt, sums, counts);
 }
 
+// compound_k with the in-plane product U*R[a,0] + V*R[a,1] reused across
+// consecutive frames whose axis columns are bit-identical (the same f64 value
+// the reference computes, so P = that + t[a] is bit-identical), 32-bit cell
+// indices (frame_cell32's quotient bounds test and truncating conversion) and
+// a 32-bit MATCH for the flush.
+template <bool kInv>
+__global__ void __launch_bounds__(256) compound2_k(ScalarFrameView fv, VoxelMap m, unsigned long long* sums,
+                                                   unsigned long long* counts) {
+  __shared__ double s_axes[kCFrames * 9];
+  __shared__ long long s_img[kCFrames];
+  __shared__ int s_same[kCFrames];
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t W = (uint32_t)fv.W, H = (uint32_t)fv.H;
+  const uint32_t tiles_u = (W + 15) / 16;
+  const uint32_t u = (blockIdx.x % tiles_u) * 16 + (warp & 1) * 8 + (lane & 7);
+  const uint32_t v = (blockIdx.x / tiles_u) * 16 + (warp >> 1) * 4 + (lane >> 3);
+  const uint32_t p = v * W + u;
+  const bool in_frame = u < W && v < H && (!fv.mask || fv.mask[p] != 0);
+  const long long hw = (long long)H * W;
+  const int64_t f0 = (int64_t)blockIdx.y * kCFrames;
+  const int nf = (int)min((int64_t)kCFrames, fv.n_frames - f0);
+  for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[f0 * 9 + i];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) s_img[i] = (long long)fv.image[f0 + i] * hw;
+  __syncthreads();
+  for (int j = threadIdx.x; j < nf; j += blockDim.x) {
+    bool same = j > 0;
+    for (int c = 0; c < 6 && same; ++c)
+      same = __double_as_longlong(s_axes[j * 9 + c]) == __double_as_longlong(s_axes[(j - 1) * 9 + c]);
+    s_same[j] = same;
+  }
+  __syncthreads();
+  const double U = (double)u * fv.px, V = (double)v * fv.py;
+  const uint32_t ny = (uint32_t)m.dims[1], nz = (uint32_t)m.dims[2];
+  double S[3] = {0.0, 0.0, 0.0};
+  int32_t cur = -1;
+  unsigned sum = 0, cnt = 0;
+  for (int j = 0; j < nf; ++j) {  // block-uniform trip count and branches
+    const double* fa = s_axes + j * 9;
+    if (!s_same[j]) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) S[a] = U * fa[a] + V * fa[3 + a];
+    }
+    bool ok = true;
+    uint32_t idx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double d = (double)__double2float_rn(S[a] + fa[6 + a]) - m.origin[a];
+      // 0 <= floor(q) < n  <=>  0 <= q < n (n integral; NaN fails both)
+      const double q = kInv ? d * m.inv_voxel : d / m.voxel;
+      ok = ok && (q >= 0.0) && (q < (double)m.dims[a]);
+      idx[a] = ok ? __double2uint_rz(q) : 0u;
+    }
+    const int32_t lin = (ok && in_frame) ? (int32_t)((idx[0] * ny + idx[1]) * nz + idx[2]) : -1;
+    const unsigned inten = in_frame ? (unsigned)fv.frames[s_img[j] + p] : 0u;
+    const bool change = lin != cur;
+    const bool need = change && cur >= 0;
+    if (__any_sync(0xffffffffu, need)) compound_flush32<false>(need, cur, sum, cnt, sums, counts);
+    if (change) {
+      cur = lin;
+      sum = 0;
+      cnt = 0;
+    }
+    sum += inten;
+    cnt += 1;
+  }
+  if (__any_sync(0xffffffffu, cur >= 0)) compound_flush32<false>(cur >= 0, cur, sum, cnt, sums, counts);
+}
+
 __global__ void compound_finalize_k(int64_t n, const unsigned long long* __restrict__ sums,
                                     const unsigned long long* __restrict__ counts, float* values,
                                     uint8_t* flags) {
@@ -510,7 +578,10 @@ extern "C" int dare_compound_accumulate(const uint8_t* frames, int64_t n_images,
           compound_tab_k<false><<<grid, 256, 0, s>>>(fv, ct, m, (unsigned long long*)d_sums,
                                                      (unsigned long long*)d_counts);
         }
-      } else
+      } else if (ncells < (int64_t)INT32_MAX && !(getenv("DARE_COMPOUND_V1") && getenv("DARE_COMPOUND_V1")[0] == '1'))
+        (m.exact_inv ? compound2_k<true> : compound2_k<false>)<<<grid, 256, 0, s>>>(
+            fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
+      else
         (m.exact_inv ? compound_k<true> : compound_k<false>)<<<grid, 256, 0, s>>>(
             fv, m, (unsigned long long*)d_sums, (unsigned long long*)d_counts);
       pt.mark("compound_k");
