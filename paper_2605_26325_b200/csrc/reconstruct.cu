@@ -668,14 +668,27 @@ struct BinOut {
 // are written back coalesced with perm.  Runs longer than kSmallRun are listed
 // for the CUB segmented-sort path; they, and the small runs of a warp that
 // has one, stay in insertion order (bins 0, perm 0).
-template <class Rec, int kRun>
-__global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(Rec rec,
+// Bulk prefetch of a warp's key segment (kBulk): one elected lane issues a
+// cp.async.bulk (TMA engine, SASS UBLKCP) of the whole 16 B-aligned segment
+// into shared memory, completing on a per-warp mbarrier, while the warp lays
+// out its cells; the staging pass then reads the keys from shared memory --
+// every key load is in flight at once instead of four per lane per round.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+template <class Rec, int kRun, bool kBulk>
+__global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? (kBulk ? 6 : 10) : 1) seal_k(Rec rec,
                                                           const uint32_t* __restrict__ offsets,
                                                           const typename Rec::Key* __restrict__ keys,
                                                           uint32_t ncells, uint4* records,
                                                           uint32_t* big_cells, uint32_t* n_big,
                                                           BinOut bo) {
+  using Key = typename Rec::Key;
+  constexpr int kRaw = kBulk ? kRun * 32 * (int)sizeof(Key) + 16 : 16;
   __shared__ SealSmem<kRun> smem[kSealWarps];
+  __shared__ __align__(16) unsigned char kraw[kSealWarps][kRaw];
+  __shared__ __align__(8) unsigned long long kbar[kSealWarps];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   SealSmem<kRun>& sm = smem[warp];
   // warp -> 32 consecutive cells of one column, z-chunk-major across warps:
@@ -699,6 +712,24 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
   const uint32_t len = s1 - s0;
   const bool staged = !__any_sync(0xffffffffu, big);  // then len <= 32 * 32
   DARE_CHECK(!staged || len <= (uint32_t)kRun * 32u);
+  uint32_t kshift = 0;  // keys of the segment start at kbuf[kshift] (16 B alignment of the copy)
+  if (kBulk && staged && len > 0) {
+    const uint32_t mb = smem_u32(&kbar[warp]);
+    const uintptr_t a = (uintptr_t)(keys + s0), a0 = a & ~(uintptr_t)15;
+    kshift = (uint32_t)((a - a0) / sizeof(Key));
+    const uint32_t bytes = (uint32_t)(((a - a0) + (uintptr_t)len * sizeof(Key) + 15) & ~(uintptr_t)15);
+    DARE_CHECK(bytes <= (uint32_t)kRaw);
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(kraw[warp])),
+          "l"(a0), "r"(bytes), "r"(mb)
+          : "memory");
+    }
+    __syncwarp();
+  }
   if (staged) {
     for (uint32_t k = 0; k < cn; ++k) sm.pos_of[cs - s0 + k] = (uint16_t)((k << 5) | lane);
     if constexpr (!Rec::kKeyBins) {
@@ -707,15 +738,27 @@ __global__ void __launch_bounds__(kSealWarps * 32, kRun <= 16 ? 10 : 1) seal_k(R
       for (int q = 0; q < 3; ++q) sm.zb[q][lane] = zbin_bound(bo.oz, bo.voxel, iz, q + 1);
     }
     __syncwarp();
+    if (kBulk && len > 0) {  // the segment has landed in shared memory
+      const uint32_t mb = smem_u32(&kbar[warp]);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(mb)
+            : "memory");
+    }
+    const Key* kbuf = reinterpret_cast<const Key*>(kraw[warp]) + kshift;
     // keys staged as u32 index + u16 (byte | z bin << 8): smaller stage, more
-    // warps.  Four loads in flight per lane; keys are read once (streaming, L1
-    // kept for the frame-axes lookups of the record pass)
+    // warps.  Four loads in flight per lane (from shared memory after the bulk
+    // prefetch); global keys are read once (streaming, L1 kept for the
+    // frame-axes lookups of the record pass)
     for (uint32_t i0 = 0; i0 < len; i0 += 128) {
-      typename Rec::Key kk[4];
+      Key kk[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t i = i0 + 32u * q + lane;
-        kk[q] = i < len ? __ldcs(keys + s0 + i) : (typename Rec::Key)0;
+        kk[q] = i < len ? (kBulk ? kbuf[i] : __ldcs(keys + s0 + i)) : (Key)0;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -960,7 +1003,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     DARE_CUDA(cudaMemsetAsync(vol->d_bins, 0, sizeof(uint32_t) * std::max<int64_t>(ncells, 1), s));
     return;
   }
-  Scratch<Key> keys(n_kept, s);
+  Scratch<Key> keys(n_kept + 4, s);  // + slack: the seal's 16 B-aligned bulk copies may read past the end
   DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * nkc, s));
   pt.mark("readback+alloc");
   if (groups > 1 && !direct) {
@@ -987,10 +1030,19 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     const char* e = getenv("DARE_SEAL_CARVEOUT");  // development override
     const int carve = e ? atoi(e) : seal_carveout;
     const int c = carve >= 0 ? carve : (int)cudaSharedmemCarveoutDefault;
-    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
-    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, kSmallRun>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, 16, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, kSmallRun, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+    DARE_CUDA(cudaFuncSetAttribute(seal_k<Rec, 16, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
   }
-  (max_run <= 16 ? seal_k<Rec, 16> : seal_k<Rec, kSmallRun>)<<<
+  // measured at cfg2: seal 1.90 ms with the bulk prefetch vs 1.73 ms without (the
+  // extra 16 KB of shared memory per block cuts residency from 10 to 6 blocks;
+  // the kernel is bound by L1 throughput, which the prefetch does not relieve) --
+  // opt-in with DARE_SEAL_BULK=1
+  const char* bulk_env = getenv("DARE_SEAL_BULK");
+  const bool bulk = bulk_env && bulk_env[0] == '1';
+  // (bulk prefetch with the 16-key stage only: the 32-key stage's buffer would
+  // exceed the 48 KB of static shared memory per block)
+  (max_run <= 16 ? (bulk ? seal_k<Rec, 16, true> : seal_k<Rec, 16, false>) : seal_k<Rec, kSmallRun, false>)<<<
       ceil_div((ncells / vol->dims[2]) * ceil_div(vol->dims[2], 32), kSealWarps), 32 * kSealWarps, 0, s>>>(
       rec, vol->d_offsets, keys.ptr, (uint32_t)ncells, vol->d_records, big_cells, n_big_d.ptr,
       BinOut{vol->origin[2], vol->voxel, vol->dims[2], vol->d_bins, vol->d_perm});

@@ -63,7 +63,8 @@ def _random_sweep(rng, n, h, w, pitch, spread):
 
 @pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
                                        ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7"), ("DARE_KEY_MODE", "0"),
-                                       ("DARE_COMPOUND_TABLES", "1"), ("DARE_COMPOUND_V1", "1")])
+                                       ("DARE_COMPOUND_TABLES", "1"), ("DARE_COMPOUND_V1", "1"),
+                                       ("DARE_SEAL_BULK", "1")])
 @pytest.mark.parametrize("key", REC_KEYS)
 def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
