@@ -15,7 +15,7 @@ timeout 900 python bench.py --config cfg4 --steps 10 --warmup 3 --no-cpu-baselin
 fi
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_cfg2.csv $CMD > gpurun_out/ev_ncu_launches.log 2>&1; echo "launches=$?" >> $S
-for spec in "reslice_fast_k:4:reslice" "frame_count_tab_k:1:count" "frame_fill_k:1:fill" "seal_k:1:seal" "compound_tab_k:1:compound" "fill_pass_k:0:fillpass" "trilinear_k:0:trilinear" "reslice_fallback_k:4:fallback" "prep_k:4:prep"; do
+for spec in "reslice_fast_k:4:reslice" "frame_count_tab_k:1:count" "frame_fill_k:1:fill" "seal_k:1:seal" "compound2_k:1:compound" "fill_pass_k:0:fillpass" "trilinear_k:0:trilinear" "reslice_fallback_k:4:fallback" "prep_k:4:prep"; do
   K=${spec%%:*}; rest=${spec#*:}; SK=${rest%%:*}; T=${rest#*:}
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$K" -s $SK -c 1 -f -o /tmp/ev_prof_$T $CMD > gpurun_out/ev_ncu_$T.log 2>&1; echo "ncu_$T=$?" >> $S
   # exports only (gpurun copies back <= 64 MiB): raw metrics, details, SASS source page of the hot kernels
