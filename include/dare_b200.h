@@ -300,6 +300,28 @@ int dare_reslice_trilinear_device(dare_scalar_t vol, int32_t n_poses, const doub
                                   int32_t width, int32_t height, uint8_t* d_pixels,
                                   uint8_t* d_coverage, double* d_values, void* stream);
 
+/* ---- evaluation --------------------------------------- */
+enum { DARE_ELEM_U8 = 0, DARE_ELEM_F64 = 1 };
+/* Replaces evaluation.py:41-84 ncc / ssim (uniform window, unbiased
+ * covariance, complete windows only) and compare_images (evaluation.py:150-160)
+ * for n_pairs image pairs a[p], b[p] of height x width (element type
+ * DARE_ELEM_U8 or DARE_ELEM_F64, [n_pairs][height][width]); a_mask / b_mask u8
+ * of the same shape or NULL (all valid).  Per pair: ncc, ssim, valid (mask
+ * intersection count) and status bits: 1 fewer than 2 valid pixels, 2 zero
+ * variance (ncc undefined), 4 no complete window, 8 image smaller than the
+ * window (ssim undefined).  SSIM is bit-identical to the reference for
+ * integer-valued images (the NCC dot products agree to rounding).  window odd
+ * and >= 3.  Host buffers; _device: device buffers on `stream`. */
+int dare_similarity(int32_t n_pairs, int32_t height, int32_t width, int32_t elem, const void* a,
+                    const uint8_t* a_mask, const void* b, const uint8_t* b_mask, int32_t window,
+                    double c1, double c2, double* ncc, double* ssim, int64_t* valid,
+                    int32_t* status);
+int dare_similarity_device(int32_t n_pairs, int32_t height, int32_t width, int32_t elem,
+                           const void* d_a, const uint8_t* d_a_mask, const void* d_b,
+                           const uint8_t* d_b_mask, int32_t window, double c1, double c2,
+                           double* d_ncc, double* d_ssim, int64_t* d_valid, int32_t* d_status,
+                           void* stream);
+
 /* ---- diagnostics -------------------------------------------------------- */
 /* Device restatement of glibc exp on n device doubles (parity tests). */
 int dare_exp_device(const double* d_x, double* d_y, int64_t n, void* stream);

@@ -402,3 +402,70 @@ def exp(x: np.ndarray) -> np.ndarray:
     y = np.empty_like(x)
     lib.oracle_exp(len(x), _a(x), _a(y))
     return y
+
+
+# ---------------------------------------------------------------- evaluation
+
+def similarity(a, b, a_mask=None, b_mask=None, window=7, c1=(0.01 * 255.0) ** 2, c2=(0.03 * 255.0) ** 2):
+    """evaluation.py:41-84 (ncc, ssim) for one 2-D pair -> (ncc, ssim, valid,
+    status) with dare_similarity's status bits (1 < 2 valid, 2 zero variance,
+    4 no complete window, 8 image smaller than the window).
+
+    Restated in the summation order the CUDA path uses, which equals the
+    reference's wherever the reference's order is fixed: window moments as row
+    sums (left to right) added top to bottom -- exact for integer-valued
+    images, so each window value is the reference's bit for bit; means and the
+    final window mean via np.sum (numpy pairwise, = the reference's np.mean);
+    the NCC dot products via np.sum of the products (the reference's np.dot is
+    BLAS, whose order is host-dependent: the tests compare that to rounding)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    mask = np.ones(a.shape, dtype=bool)
+    for m in (a_mask, b_mask):
+        if m is not None:
+            mask &= np.asarray(m, dtype=bool)
+    status = 0
+    va, vb = a[mask], b[mask]
+    n = va.size
+    nc = 0.0
+    if n < 2:
+        status |= 1
+    else:
+        da = va - np.sum(va) / n
+        db = vb - np.sum(vb) / n
+        den = math.sqrt(float(np.sum(da * da)) * float(np.sum(db * db)))
+        if den == 0.0:
+            status |= 2
+        else:
+            nc = float(np.sum(da * db)) / den
+    H, W = a.shape
+    ss = 0.0
+    if H < window or W < window:
+        status |= 8
+    else:
+        HH, WW = H - window + 1, W - window + 1
+        mf = mask.astype(np.float64)
+        rows = [np.zeros((H, WW)) for _ in range(6)]
+        for dx in range(window):
+            sl = np.s_[:, dx:dx + WW]
+            p, q = a[sl], b[sl]
+            for k, v in enumerate((p, q, p * p, q * q, p * q, mf[sl])):
+                rows[k] = rows[k] + v
+        s = [np.zeros((HH, WW)) for _ in range(6)]
+        for dy in range(window):
+            for k in range(6):
+                s[k] = s[k] + rows[k][dy:dy + HH]
+        nn = float(window * window)
+        norm = nn / (nn - 1.0)
+        mu_a, mu_b = s[0] / nn, s[1] / nn
+        var_a = norm * (s[2] / nn - mu_a * mu_a)
+        var_b = norm * (s[3] / nn - mu_b * mu_b)
+        cov = norm * (s[4] / nn - mu_a * mu_b)
+        val = ((2.0 * mu_a * mu_b + c1) * (2.0 * cov + c2)) / ((mu_a * mu_a + mu_b * mu_b + c1) * (var_a + var_b + c2))
+        complete = s[5] == nn
+        if not complete.any():
+            status |= 4
+        else:
+            sel = val[complete]
+            ss = float(np.sum(sel)) / sel.size
+    return nc, ss, n, status

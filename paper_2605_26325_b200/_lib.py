@@ -116,6 +116,10 @@ _SIGNATURES = {
     "dare_fill_holes": [c_vp, c_i32, ctypes.POINTER(c_vp), P_i32],
     "dare_reslice_trilinear": [c_vp, c_i32, P_f64, c_i32, c_i32, P_u8, P_u8, P_f64],
     "dare_reslice_trilinear_device": [c_vp, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp],
+    "dare_similarity": [c_i32, c_i32, c_i32, c_i32, c_vp, P_u8, c_vp, P_u8, c_i32, c_f64, c_f64, P_f64, P_f64,
+                        P_i64, P_i32],
+    "dare_similarity_device": [c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_f64, c_vp,
+                               c_vp, c_vp, c_vp, c_vp],
     "dare_exp_device": [c_vp, c_vp, c_i64, c_vp],
     "dare_reslice_last_fallback": [P_i64],
     "dare_fastmath_check": [P_f64, P_f64, P_i32],
