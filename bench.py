@@ -453,7 +453,65 @@ def scalar_arm_bench(db, wl, dev_sweep, frames_d, planes, peak, torch):
         "trilinear": {"ms_per_batch": ms_t, "poses": len(planes), "reslices_per_s": len(planes) / (ms_t / 1000.0),
                       "note": "host-buffer C-ABI call incl. pose upload and image download"},
         "timing": "best of 4 calls after a warm-up call (each synchronises)",
-    }
+    }, filled
+
+
+def evaluation_bench(db, vol, filled, planes, cfg, torch):
+    """The reference CLI benchmark's evaluation loop (cli.py:253-287, SURVEY
+    8f row 4) on this step's planes: directional reslices and trilinear
+    baseline reslices compared with the noise-free phantom rendered at each
+    plane (phantom.ground_truth_reslice), the 2P (NCC, SSIM) metrics in one
+    dare_similarity launch on device tensors; medians and paired Wilcoxon p
+    from run_comparison.  CPU: the oracle's numpy restatement per pair."""
+    from paper_2605_26325_b200 import evaluation as ev
+    from paper_2605_26325_b200.reslice import ResliceImage
+
+    from oracle import oracle
+
+    W, H = planes[0].width, planes[0].height
+    truth = bench_data.render_phantom([p.pose for p in planes], W, H, planes[0].pixel_pitch, None, noise=False)
+    dp, dc, _ = db.reslice_batch(vol, planes, cfg)
+    bp, bc, _ = db.reslice_trilinear_batch(filled, planes)
+    a = torch.from_numpy(np.concatenate([dp, bp])).cuda()
+    am = torch.from_numpy(np.concatenate([dc, bc])).cuda()
+    t2 = torch.cat([truth, truth])
+    ev.similarity_batch(a, t2, am, None)  # warm-up
+    best_dev = best_wall = None
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        r = ev.similarity_batch(a, t2, am, None)  # returns after the results' D2H
+        e1.record()
+        e1.synchronize()
+        wall = (time.perf_counter() - t0) * 1000.0
+        dev = e0.elapsed_time(e1)
+        best_dev = dev if best_dev is None else min(best_dev, dev)
+        best_wall = wall if best_wall is None else min(best_wall, wall)
+    th = truth.cpu().numpy()
+    ones = np.ones((H, W), bool)
+    T = [ResliceImage(pixels=th[k], coverage=ones, timing_ms=0.0) for k in range(len(planes))]
+    A = [ResliceImage(pixels=dp[k], coverage=dc[k], timing_ms=0.0) for k in range(len(planes))]
+    B = [ResliceImage(pixels=bp[k], coverage=bc[k], timing_ms=0.0) for k in range(len(planes))]
+    rep = ev.run_comparison(A, B, T)
+    t0 = time.perf_counter()
+    ncpu = 2
+    for k in range(ncpu):
+        o = oracle.similarity(dp[k], th[k], dc[k], None)
+    cpu_ms = (time.perf_counter() - t0) * 1000.0 / ncpu
+    parity = bool(o[0] == r.ncc[ncpu - 1] and o[1] == r.ssim[ncpu - 1])
+    n = 2 * len(planes)
+    s = rep.summary
+    return {"pairs": n, "raster": f"{W}x{H}", "device_ms": best_dev, "wall_ms": best_wall,
+            "pairs_per_s": n / (best_dev / 1000.0),
+            "cpu_baseline": {"ms_per_pair": cpu_ms, "kind": "port", "cores": 1,
+                             "sample": f"{ncpu} pairs through oracle.similarity (numpy)",
+                             "parity_with_gpu": parity},
+            "median": {m: {k: s[m][k]["median"] for k in ("dare", "baseline")} for m in ("ncc", "ssim")},
+            "wilcoxon_p": {m: s[m]["wilcoxon_p"] for m in ("ncc", "ssim")},
+            "excluded_pairs": len(s["excluded_pairs"]),
+            "note": "truth = noise-free phantom at each plane (bench_data.render_phantom, noise=False); "
+                    "device_ms = CUDA events around similarity_batch on device tensors (best of 4)"}
 
 
 def service_bench(vol, planes, cfg, clients: int = 8):
@@ -805,9 +863,12 @@ def run_b200(args):
     achieved = ref_bytes / (ms_per_step / 1000.0) / 1e9
 
     # ---- direction-blind arm (config 5): compound -> fill_holes -> trilinear ----
-    scalar_arm = None
+    scalar_arm = evaluation = None
     if rank == 0 and not args.no_scalar:
-        scalar_arm = scalar_arm_bench(db, wl, dev_sweep, frames_d, planes[step0 * B:(step0 + 1) * B], peak, torch)
+        step_planes = planes[step0 * B:(step0 + 1) * B]
+        scalar_arm, filled = scalar_arm_bench(db, wl, dev_sweep, frames_d, step_planes, peak, torch)
+        evaluation = evaluation_bench(db, vol, filled, step_planes, cfg, torch)
+        del filled
 
     # ---- CPU baseline (rank 0, bounded sample) ----
     cpu = recon_cpu = None
@@ -866,7 +927,7 @@ def run_b200(args):
             "certified": certified,
             "clocks": clk,
             "cpu_baseline": cpu,
-            "scalar_arm": scalar_arm, "service": service,
+            "scalar_arm": scalar_arm, "service": service, "evaluation": evaluation,
         }
         print(json.dumps(out))
     if dist is not None:

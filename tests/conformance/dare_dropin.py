@@ -12,6 +12,9 @@ the package __init__):
   reslice            (reslice.py:168-187)       -> paper_2605_26325_b200.reslice
   compound / fill_holes / reslice_trilinear (baseline.py:64-155)
                                                 -> paper_2605_26325_b200.scalar.*
+  ncc / ssim / compare_images / run_comparison / wilcoxon_signed_rank /
+  latency_stats / time_reslice / write_report / format_summary
+  (evaluation.py:41-355)                        -> paper_2605_26325_b200.evaluation.*
 
 The service module's isinstance test of the volume kind (service.py:32,202)
 is widened to accept the drop-in's DirectionalVolume.
@@ -19,7 +22,8 @@ reslice_bruteforce stays the reference's numba kernel, so the reference's
 oracle-equivalence tests (test_reslice.py:152-179, acceptance criterion 1)
 compare the GPU path against the reference's own brute force.  Test files are
 the reference's, unmodified; scikit-image (absent from the image) is stubbed
-for import only, and the SSIM-based criteria are deselected by the runner.
+for import only, and the tests that call it (SSIM vs skimage) are deselected
+by the runner.
 """
 from __future__ import annotations
 
@@ -63,7 +67,7 @@ def pytest_configure(config):
     import dare.volume
 
     import paper_2605_26325_b200 as b200
-    from paper_2605_26325_b200 import _lib, scalar
+    from paper_2605_26325_b200 import _lib, evaluation, scalar
 
     if not os.environ.get("DARE_DROPIN_DRYRUN"):  # (collection check without a GPU)
         _lib.init(0)
@@ -74,6 +78,9 @@ def pytest_configure(config):
         "fill_holes": scalar.fill_holes,
         "reslice_trilinear": scalar.reslice_trilinear,
     }
+    for name in ("ncc", "ssim", "compare_images", "run_comparison", "wilcoxon_signed_rank", "latency_stats",
+                 "time_reslice", "write_report", "format_summary"):
+        repl[name] = getattr(evaluation, name)
     for mod in (dare, dare.reconstruct, dare.reslice, dare.baseline, dare.cli, dare.service, dare.evaluation):
         for name, fn in repl.items():
             if hasattr(mod, name):
