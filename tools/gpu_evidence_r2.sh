@@ -10,8 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_s
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/ev_bench_cfg2.json 2> gpurun_out/ev_bench_cfg2.err; echo "bench=$?" >> $S
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/ev_bench_ref_cfg2.json 2> gpurun_out/ev_bench_ref_cfg2.err; echo "ref=$?" >> $S
 timeout 600 python bench.py --config cfg1 --steps 20 --warmup 5 > gpurun_out/ev_bench_cfg1.json 2> gpurun_out/ev_bench_cfg1.err; echo "cfg1=$?" >> $S
-timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_cfg3.json 2> gpurun_out/ev_bench_cfg3.err; echo "cfg3=$?" >> $S
-timeout 900 python bench.py --config cfg4 --steps 10 --warmup 3 --no-cpu-baseline --no-scalar > gpurun_out/ev_bench_cfg4.json 2> gpurun_out/ev_bench_cfg4.err; echo "cfg4=$?" >> $S
+timeout 1500 python bench.py --config cfg3 --steps 10 --warmup 3 > gpurun_out/ev_bench_cfg3.json 2> gpurun_out/ev_bench_cfg3.err; echo "cfg3=$?" >> $S
+timeout 1500 python bench.py --config cfg4 --steps 10 --warmup 3 --no-scalar > gpurun_out/ev_bench_cfg4.json 2> gpurun_out/ev_bench_cfg4.err; echo "cfg4=$?" >> $S
 fi
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_cfg2.csv $CMD > gpurun_out/ev_ncu_launches.log 2>&1; echo "launches=$?" >> $S
