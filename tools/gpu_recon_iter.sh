@@ -10,3 +10,5 @@ if [ $rc -ne 0 ]; then tail -30 gpurun_out/pytest_$T.log; cat $S; exit 1; fi
 DARE_PROFILE=1 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-scalar > gpurun_out/bench_${T}_cfg2.json 2> gpurun_out/bench_${T}_cfg2.err; echo "cfg2=$?" >> $S
 DARE_PROFILE=1 timeout 900 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline --no-scalar > gpurun_out/bench_${T}_cfg3.json 2> gpurun_out/bench_${T}_cfg3.err; echo "cfg3=$?" >> $S
 cat $S
+DARE_FILL_V1=1 DARE_PROFILE=1 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-scalar > gpurun_out/bench_${T}_cfg2_v1.json 2> gpurun_out/bench_${T}_cfg2_v1.err; echo "cfg2_v1=$?" >> $S
+DARE_FILL_V1=1 DARE_PROFILE=1 timeout 900 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline --no-scalar > gpurun_out/bench_${T}_cfg3_v1.json 2> gpurun_out/bench_${T}_cfg3_v1.err; echo "cfg3_v1=$?" >> $S
