@@ -72,13 +72,21 @@ __device__ inline bool pw_node(int64_t n, int d, int64_t k, int64_t& off, int64_
 
 // K parallel sums over i in [0, n) of f(i)[0..K) in numpy's pairwise order.
 // S: 2^D x K doubles of scratch (D = pw_depth(n)); the result lands in S[0..K).
+// Leaves are summed by groups of 8 lanes: lane u keeps numpy's accumulator
+// r[u] (elements u, u+8, ... of the leaf, so each step's 8 loads are one
+// coalesced 64 B segment), the group combines ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) with shuffles in exactly that association, and lane 0
+// adds the tail.
 template <int K, class Fn>
 __device__ void pw_reduce(int64_t n, Fn f, double* S) {
   const int D = pw_depth(n);
   const int64_t slots = (int64_t)1 << D;
+  const uint32_t lane = threadIdx.x & 31u, u = lane & 7u;
+  const unsigned gmask = 0xffu << (lane & ~7u);
+  const int64_t groups = blockDim.x >> 3;
   // leaves: slot j represents the leaf containing it if j's bits below the
   // leaf's depth are zero
-  for (int64_t j = threadIdx.x; j < slots; j += blockDim.x) {
+  for (int64_t j = threadIdx.x >> 3; j < slots; j += groups) {
     int64_t off = 0, len = n;
     int d = 0;
     while (len > kLeaf) {
@@ -91,43 +99,49 @@ __device__ void pw_reduce(int64_t n, Fn f, double* S) {
       }
       ++d;
     }
-    if (d < D && (j & ((((int64_t)1) << (D - d)) - 1)) != 0) continue;
+    if (d < D && (j & ((((int64_t)1) << (D - d)) - 1)) != 0) continue;  // group-uniform
     double res[K];
     if (len < 8) {
+      if (u == 0) {
 #pragma unroll
-      for (int c = 0; c < K; ++c) res[c] = -0.0;
-      for (int64_t i = 0; i < len; ++i) {
-        double v[K];
-        f(off + i, v);
-#pragma unroll
-        for (int c = 0; c < K; ++c) res[c] += v[c];
-      }
-    } else {
-      double r[8][K];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) f(off + u, r[u]);
-      int64_t i = 8;
-      for (; i < len - (len % 8); i += 8) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int c = 0; c < K; ++c) res[c] = -0.0;
+        for (int64_t i = 0; i < len; ++i) {
           double v[K];
-          f(off + i + u, v);
+          f(off + i, v);
 #pragma unroll
-          for (int c = 0; c < K; ++c) r[u][c] += v[c];
+          for (int c = 0; c < K; ++c) res[c] += v[c];
         }
-      }
 #pragma unroll
-      for (int c = 0; c < K; ++c)
-        res[c] = ((r[0][c] + r[1][c]) + (r[2][c] + r[3][c])) + ((r[4][c] + r[5][c]) + (r[6][c] + r[7][c]));
-      for (; i < len; ++i) {
-        double v[K];
-        f(off + i, v);
-#pragma unroll
-        for (int c = 0; c < K; ++c) res[c] += v[c];
+        for (int c = 0; c < K; ++c) S[j * K + c] = res[c];
       }
+      continue;
+    }
+    double r[K];
+    f(off + u, r);
+    const int64_t body = len - (len % 8);
+    for (int64_t i = 8; i < body; i += 8) {
+      double v[K];
+      f(off + i + u, v);
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[c] += v[c];
     }
 #pragma unroll
-    for (int c = 0; c < K; ++c) S[j * K + c] = res[c];
+    for (int c = 0; c < K; ++c) {
+      double x = r[c] + __shfl_down_sync(gmask, r[c], 1, 8);  // u even: r_u + r_{u+1}
+      x = x + __shfl_down_sync(gmask, x, 2, 8);               // u % 4 == 0: (..) + (..)
+      x = x + __shfl_down_sync(gmask, x, 4, 8);               // u == 0: the full combination
+      res[c] = x;
+    }
+    if (u == 0) {
+      for (int64_t i = body; i < len; ++i) {
+        double v[K];
+        f(off + i, v);
+#pragma unroll
+        for (int c = 0; c < K; ++c) res[c] += v[c];
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) S[j * K + c] = res[c];
+    }
   }
   __syncthreads();
   // combine bottom-up: an internal node (d, k) adds its right child's sum
@@ -219,7 +233,8 @@ __global__ void __launch_bounds__(128) ssim_window_k(const T* __restrict__ a, co
   // evaluation.py:73-80: n = window*window, unbiased norm n / (n - 1.0)
   const double n = (double)(win * win);
   const double norm = n / (n - 1.0);
-  for (int r = y0; r < y1 + win - 1; ++r) {
+  int slot = 0;  // (r - y0) mod win, kept incrementally
+  for (int r = y0; r < y1 + win - 1; ++r, slot = slot + 1 == win ? 0 : slot + 1) {
     __syncthreads();
     for (int i = tid; i < span; i += nt) {
       const int c = x0 + i;
@@ -245,14 +260,13 @@ __global__ void __launch_bounds__(128) ssim_window_k(const T* __restrict__ a, co
       h[4] += p * q;
       h[5] += st[2 * span + tid + j];
     }
-    const int slot = (r - y0) % win;
 #pragma unroll
     for (int c = 0; c < 6; ++c) ring[((size_t)slot * 6 + c) * nt + tid] = h[c];
     const int y = r - (win - 1);
     if (y >= y0 && x < WW) {
       double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      for (int j = 0; j < win; ++j) {
-        const int sl = (y - y0 + j) % win;
+      // rows y .. r in order: row y's slot follows row r's in the ring of win
+      for (int j = 0, sl = slot + 1 == win ? 0 : slot + 1; j < win; ++j, sl = sl + 1 == win ? 0 : sl + 1) {
 #pragma unroll
         for (int c = 0; c < 6; ++c) s[c] += ring[((size_t)sl * 6 + c) * nt + tid];
       }
@@ -270,74 +284,187 @@ __global__ void __launch_bounds__(128) ssim_window_k(const T* __restrict__ a, co
   }
 }
 
-// One CTA per pair: NCC over the mask intersection (evaluation.py:41-53),
-// then the mean of the complete windows' SSIM values (evaluation.py:82).
+// u8 images: integer window moments (exact and order-free, so equal to
+// ssim_window_k's f64 sums) kept as running column sums -- each image row adds
+// its 7-wide row sums, and the row leaving the window subtracts the sums it
+// added (an int ring of the last win + 1 rows' sums, 24 KB at win 7, instead
+// of the 43 KB f64 ring).  The next image row is fetched into registers while
+// the current one is summed; the f64 SSIM expression runs only for complete
+// windows (the others are never averaged).
+template <int kWin>  // the window at compile time (7, the default), or 0: `win`
+__global__ void __launch_bounds__(128) ssim_window_u8_k(const uint8_t* __restrict__ a,
+                                                        const uint8_t* __restrict__ am,
+                                                        const uint8_t* __restrict__ b,
+                                                        const uint8_t* __restrict__ bm, int H, int W, int win_rt,
+                                                        double c1, double c2, double* __restrict__ V,
+                                                        uint8_t* __restrict__ F) {
+  const int win = kWin ? kWin : win_rt;
+  extern __shared__ uint8_t sb[];  // [win + 1 rows][3][span]
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int HH = H - win + 1, WW = W - win + 1;
+  const int64_t pair = blockIdx.z;
+  const int x0 = blockIdx.x * nt, x = x0 + tid;
+  const int y0 = blockIdx.y * kBand;
+  if (y0 >= HH) return;
+  const int y1 = min(y0 + kBand, HH);
+  const int span = nt + win - 1, R = win + 1;
+  int* hring = reinterpret_cast<int*>(sb + (((size_t)R * 3 * span + 15) & ~(size_t)15));  // [R][6][nt]
+  const size_t base = (size_t)pair * H * W;
+  const double n = (double)(win * win);
+  const double norm = n / (n - 1.0);
+  int S[6] = {0, 0, 0, 0, 0, 0};
+  // a thread stages columns tid and tid + nt of each row (span <= 2 nt);
+  // row r + 1 is loaded into registers while row r is summed
+  auto fetch = [&](int r, uint32_t (&w)[2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = tid + h * nt, c = x0 + i;
+      w[h] = 0u;
+      if (i < span && c < W) {
+        const size_t k = base + (size_t)r * W + c;
+        w[h] = (uint32_t)a[k] | ((uint32_t)b[k] << 8) | ((valid_at(am, bm, k) ? 1u : 0u) << 16);
+      }
+    }
+  };
+  const int r_end = y1 + win - 1;
+  uint32_t nxt[2];
+  fetch(y0, nxt);
+  int slot = 0;  // ring slot of row r: (r - y0) mod R, kept incrementally (no integer division)
+  for (int r = y0; r < r_end; ++r, slot = slot + 1 == R ? 0 : slot + 1) {
+    const uint32_t cur[2] = {nxt[0], nxt[1]};
+    if (r + 1 < r_end) fetch(r + 1, nxt);
+    uint8_t* row = sb + (size_t)slot * 3 * span;
+    __syncthreads();  // the slot's previous row (r - R) was last read at r - 1
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = tid + h * nt;
+      if (i < span) {
+        row[i] = (uint8_t)cur[h];
+        row[span + i] = (uint8_t)(cur[h] >> 8);
+        row[2 * span + i] = (uint8_t)(cur[h] >> 16);
+      }
+    }
+    __syncthreads();
+    // this row's 7-wide sums enter the window and are kept in the int ring;
+    // the sums of the row leaving (r - win) come back from it
+    int h[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < (kWin ? kWin : win); ++j) {
+      const int p = row[tid + j], q = row[span + tid + j];
+      h[0] += p;
+      h[1] += q;
+      h[2] += p * p;
+      h[3] += q * q;
+      h[4] += p * q;
+      h[5] += row[2 * span + tid + j];
+    }
+    int* hr = hring + (size_t)slot * 6 * nt + tid;
+    const int* ho = hring + (size_t)(slot + 1 == R ? 0 : slot + 1) * 6 * nt + tid;  // row r - win
+    const bool leave = r - y0 >= win;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      S[c] += h[c] - (leave ? ho[c * nt] : 0);
+      hr[c * nt] = h[c];
+    }
+    const int y = r - (win - 1);
+    if (y >= y0 && x < WW) {
+      const size_t o = (size_t)pair * HH * WW + (size_t)y * WW + x;
+      const bool complete = S[5] == win * win;
+      F[o] = complete;
+      if (complete) {  // only complete windows are averaged (evaluation.py:82)
+        double s[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) s[c] = (double)S[c];
+        const double mu_a = s[0] / n, mu_b = s[1] / n;
+        const double var_a = norm * (s[2] / n - mu_a * mu_a);
+        const double var_b = norm * (s[3] / n - mu_b * mu_b);
+        const double cov = norm * (s[4] / n - mu_a * mu_b);
+        const double num = (2.0 * mu_a * mu_b + c1) * (2.0 * cov + c2);
+        const double den = (mu_a * mu_a + mu_b * mu_b + c1) * (var_a + var_b + c2);
+        V[o] = num / den;
+      }
+    }
+  }
+}
+
+// Per pair two CTAs: blockIdx.y == 0 computes NCC over the mask intersection
+// (evaluation.py:41-53) and the valid count, blockIdx.y == 1 the mean of the
+// complete windows' SSIM values (evaluation.py:82).  Scratch per pair: A, B
+// (masked values), C (complete window values), S (reduction slots, 4 x 2^D).
 template <class T>
 __global__ void __launch_bounds__(kReduceThreads) sim_reduce_k(
     const T* __restrict__ a, const uint8_t* __restrict__ am, const T* __restrict__ b,
     const uint8_t* __restrict__ bm, int H, int W, int win, int do_ssim, const double* __restrict__ V,
-    const uint8_t* __restrict__ F, double* __restrict__ scratch, int64_t scratch_per_pair,
+    const uint8_t* __restrict__ F, double* __restrict__ scratch, int64_t scratch_per_pair, int64_t slots,
     double* __restrict__ ncc_out, double* __restrict__ ssim_out, int64_t* __restrict__ valid_out,
     int32_t* __restrict__ status_out) {
   const int64_t pair = blockIdx.x;
   const int64_t HW = (int64_t)H * W;
-  double* A = scratch + pair * scratch_per_pair;
-  double* B = A + HW;
-  double* S = B + HW;
-  const size_t base = (size_t)pair * HW;
-  const int64_t n = compact(
-      HW, [&](int64_t i) { return valid_at(am, bm, base + i); },
-      [&](int64_t i, int64_t p) {
-        A[p] = ld(a, base + i);
-        B[p] = ld(b, base + i);
-      });
-  int32_t status = 0;
-  double ncc = 0.0;
-  if (n < 2) {
-    status |= 1;  // "ncc needs at least 2 mutually valid pixels"
-  } else {
-    __syncthreads();
-    pw_reduce<2>(n, [&](int64_t i, double* v) { v[0] = A[i]; v[1] = B[i]; }, S);
-    const double ma = S[0] / (double)n, mb = S[1] / (double)n;  // va.mean(), vb.mean()
-    __syncthreads();
-    pw_reduce<3>(
-        n,
-        [&](int64_t i, double* v) {
-          const double da = A[i] - ma, db = B[i] - mb;
-          v[0] = da * da;
-          v[1] = db * db;
-          v[2] = da * db;
-        },
-        S);
-    const double denom = sqrt(S[0] * S[1]);
-    if (denom == 0.0)
-      status |= 2;  // "ncc undefined for zero-variance input"
-    else
-      ncc = S[2] / denom;
+  const int64_t WN = do_ssim ? (int64_t)(H - win + 1) * (W - win + 1) : 0;
+  // masked values compacted in their input type (u8: 1 B each), converted on read
+  double* C = scratch + pair * scratch_per_pair;
+  double* S = C + WN + (blockIdx.y ? 3 * slots : 0);
+  T* A = reinterpret_cast<T*>(C + WN + 4 * slots);
+  T* B = A + HW;
+  if (blockIdx.y == 0) {
+    const size_t base = (size_t)pair * HW;
+    const int64_t n = compact(
+        HW, [&](int64_t i) { return valid_at(am, bm, base + i); },
+        [&](int64_t i, int64_t p) {
+          A[p] = a[base + i];
+          B[p] = b[base + i];
+        });
+    int32_t status = 0;
+    double ncc = 0.0;
+    if (n < 2) {
+      status |= 1;  // "ncc needs at least 2 mutually valid pixels"
+    } else {
+      __syncthreads();
+      pw_reduce<2>(n, [&](int64_t i, double* v) { v[0] = (double)A[i]; v[1] = (double)B[i]; }, S);
+      const double ma = S[0] / (double)n, mb = S[1] / (double)n;  // va.mean(), vb.mean()
+      __syncthreads();
+      pw_reduce<3>(
+          n,
+          [&](int64_t i, double* v) {
+            const double da = (double)A[i] - ma, db = (double)B[i] - mb;
+            v[0] = da * da;
+            v[1] = db * db;
+            v[2] = da * db;
+          },
+          S);
+      const double denom = sqrt(S[0] * S[1]);
+      if (denom == 0.0)
+        status |= 2;  // "ncc undefined for zero-variance input"
+      else
+        ncc = S[2] / denom;
+    }
+    if (threadIdx.x == 0) {
+      ncc_out[pair] = ncc;
+      valid_out[pair] = n;
+      atomicOr(status_out + pair, status);
+    }
+    return;
   }
+  int32_t status = 0;
   double ssim = 0.0;
   if (do_ssim) {
-    __syncthreads();
-    const int64_t WN = (int64_t)(H - win + 1) * (W - win + 1);
     const double* Vp = V + pair * WN;
     const uint8_t* Fp = F + pair * WN;
     const int64_t m = compact(
-        WN, [&](int64_t i) { return Fp[i] != 0; }, [&](int64_t i, int64_t p) { A[p] = Vp[i]; });
+        WN, [&](int64_t i) { return Fp[i] != 0; }, [&](int64_t i, int64_t p) { C[p] = Vp[i]; });
     if (m == 0) {
       status |= 4;  // "no complete ssim window inside the mask intersection"
     } else {
       __syncthreads();
-      pw_reduce<1>(m, [&](int64_t i, double* v) { v[0] = A[i]; }, S);
+      pw_reduce<1>(m, [&](int64_t i, double* v) { v[0] = C[i]; }, S);
       ssim = S[0] / (double)m;
     }
   } else {
     status |= 8;  // image smaller than the window: no SSIM
   }
   if (threadIdx.x == 0) {
-    ncc_out[pair] = ncc;
     ssim_out[pair] = ssim;
-    valid_out[pair] = n;
-    status_out[pair] = status;
+    atomicOr(status_out + pair, status);
   }
 }
 
@@ -345,11 +472,13 @@ template <class T>
 void launch_similarity(int32_t P, int32_t H, int32_t W, const T* a, const uint8_t* am, const T* b,
                        const uint8_t* bm, int32_t win, double c1, double c2, double* ncc, double* ssim,
                        int64_t* valid, int32_t* status, cudaStream_t s) {
+  constexpr bool kU8 = sizeof(T) == 1;
   const int64_t HW = (int64_t)H * W;
   const bool do_ssim = H >= win && W >= win;
   const int64_t WN = do_ssim ? (int64_t)(H - win + 1) * (W - win + 1) : 0;
   const int64_t slots = (int64_t)1 << std::max(pw_depth(HW), pw_depth(std::max<int64_t>(WN, 1)));
-  const int64_t per_pair = 2 * HW + 3 * slots;
+  // doubles per pair: C (WN) + slots (4 x 2^D) + the compacted a, b values (2 HW of T, 8 B aligned)
+  const int64_t per_pair = WN + 4 * slots + (2 * HW * (int64_t)sizeof(T) + 7) / 8;
   // bound the scratch: pairs per launch so that values + flags + reductions
   // stay under ~1 GB
   const int64_t bytes_pair = per_pair * 8 + WN * 9;
@@ -357,12 +486,20 @@ void launch_similarity(int32_t P, int32_t H, int32_t W, const T* a, const uint8_
   Scratch<double> scr((size_t)chunk * per_pair, s);
   Scratch<double> vals((size_t)chunk * WN, s);
   Scratch<uint8_t> flags((size_t)chunk * WN, s);
-  const int nt = win <= 31 ? 128 : 32;
-  const size_t smem = ((size_t)win * 6 * nt + 3 * (size_t)(nt + win - 1)) * sizeof(double);
+  const int nt = kU8 ? 128 : (win <= 31 ? 128 : 32);
+  const size_t smem = kU8 ? (((size_t)(win + 1) * 3 * (nt + win - 1) + 15) & ~(size_t)15) +
+                                (size_t)(win + 1) * 6 * nt * sizeof(int)
+                          : ((size_t)win * 6 * nt + 3 * (size_t)(nt + win - 1)) * sizeof(double);
+  using WindowFn = void (*)(const T*, const uint8_t*, const T*, const uint8_t*, int, int, int, double, double,
+                            double*, uint8_t*);
+  auto window_kernel = kU8 ? (win == 7 ? (WindowFn)ssim_window_u8_k<7> : (WindowFn)ssim_window_u8_k<0>)
+                           : ssim_window_k<T>;
   if (do_ssim) {
-    DARE_LIMIT(smem <= 220 * 1024, "ssim window too large (at most 127)");
-    DARE_CUDA(cudaFuncSetAttribute(ssim_window_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DARE_LIMIT(smem <= 220 * 1024 && win <= 127, "ssim window too large (at most 127)");
+    DARE_CUDA(cudaFuncSetAttribute((const void*)window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
   }
+  DARE_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * (size_t)P, s));
   for (int32_t p0 = 0; p0 < P; p0 += chunk) {
     const int32_t np = std::min(chunk, P - p0);
     const size_t off = (size_t)p0 * HW;
@@ -373,15 +510,16 @@ void launch_similarity(int32_t P, int32_t H, int32_t W, const T* a, const uint8_
       const size_t qo = (size_t)q0 * HW;
       if (do_ssim) {
         dim3 grid(ceil_div(W - win + 1, nt), ceil_div(H - win + 1, kBand), nq);
-        ssim_window_k<T><<<grid, nt, smem, s>>>(a + off + qo, amp ? amp + qo : nullptr, b + off + qo,
-                                                bmp ? bmp + qo : nullptr, H, W, win, c1, c2,
-                                                vals.ptr + (size_t)q0 * WN, flags.ptr + (size_t)q0 * WN);
+        window_kernel<<<grid, nt, smem, s>>>(a + off + qo, amp ? amp + qo : nullptr, b + off + qo,
+                                             bmp ? bmp + qo : nullptr, H, W, win, c1, c2,
+                                             vals.ptr + (size_t)q0 * WN, flags.ptr + (size_t)q0 * WN);
         DARE_CUDA(cudaGetLastError());
       }
     }
-    sim_reduce_k<T><<<np, kReduceThreads, 0, s>>>(a + off, amp, b + off, bmp, H, W, win, do_ssim ? 1 : 0,
-                                                  vals.ptr, flags.ptr, scr.ptr, per_pair, ncc + p0,
-                                                  ssim + p0, valid + p0, status + p0);
+    sim_reduce_k<T><<<dim3(np, 2), kReduceThreads, 0, s>>>(a + off, amp, b + off, bmp, H, W, win,
+                                                           do_ssim ? 1 : 0, vals.ptr, flags.ptr, scr.ptr,
+                                                           per_pair, slots, ncc + p0, ssim + p0, valid + p0,
+                                                           status + p0);
     DARE_CUDA(cudaGetLastError());
   }
 }
@@ -394,6 +532,7 @@ void similarity_device(int32_t P, int32_t H, int32_t W, int32_t elem, const void
   DARE_REQUIRE(elem == DARE_ELEM_U8 || elem == DARE_ELEM_F64, "element type must be u8 or f64");
   DARE_LIMIT((int64_t)H * W <= ((int64_t)1 << 31), "image too large");
   if (P == 0) return;
+  (void)thread_stream();  // first call on this device: keeps the scratch pool (release threshold)
   if (elem == DARE_ELEM_U8)
     launch_similarity<uint8_t>(P, H, W, (const uint8_t*)a, am, (const uint8_t*)b, bm, win, c1, c2, ncc, ssim,
                                valid, status, s);
