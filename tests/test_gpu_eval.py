@@ -69,6 +69,17 @@ def test_masked_f64_and_windows(rng):
         _check_batch_vs_oracle(a, b, am, None, win)
 
 
+def test_u8_windows(rng):
+    """The u8 window kernel (integer running sums) for compile-time 7 and runtime windows."""
+    for win in (3, 5, 7, 9, 15, 33, 63):
+        h, w = int(rng.integers(win, win + 90)), int(rng.integers(win, win + 140))
+        a = rng.integers(0, 256, (2, h, w)).astype(np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-25, 26, a.shape), 0, 255).astype(np.uint8)
+        am = rng.random(a.shape) < 0.998
+        bm = rng.random(a.shape) < 0.999
+        _check_batch_vs_oracle(a, b, am, bm, win)
+
+
 def test_u8_batch_full_size(rng):
     """64 reslice-sized (256x256) u8 pairs with coverage masks in one launch,
     plus a 512x512 pair."""

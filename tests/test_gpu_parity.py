@@ -572,3 +572,56 @@ def test_split_pixel_variants_identical(rng, parts, monkeypatch):
             ref = oracle.reslice(vol, oracle.plane_params(planes[k]), oracle.cfg_array(cfg), 37, 29)
             np.testing.assert_array_equal(px[k], ref[0])
             np.testing.assert_array_equal(cov[k], ref[1])
+
+
+def _few_orient_volume(rng, n, k, extent=10.0, voxel=0.5):
+    """Samples sharing k distinct orientations (sweeps at fixed probe
+    orientations), so the direction-cluster index applies (k <= 1024)."""
+    b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (extent,) * 3), voxel)
+    qs = rng.normal(size=(k, 4))
+    qs /= np.linalg.norm(qs, axis=1, keepdims=True)
+    qs[qs[:, 0] < 0] *= -1.0
+    pos = rng.uniform(0, extent, (n, 3))
+    b.insert_batch(pos, qs[rng.integers(0, k, n)], rng.integers(0, 256, n))
+    return b.seal(), qs
+
+
+@pytest.mark.parametrize("k", [2, 3, 6, 17, 200])
+def test_direction_cluster_index_identical(rng, k, monkeypatch):
+    """The certified path over the direction-cluster index (split.cu: only the
+    clusters a pose accepts are walked) equals the exact FP64 path, the
+    certified path on the canonical layout (DARE_ORIENT_SPLIT=0, a second copy
+    of the volume) and the oracle, for planes aligned with the volume's
+    orientations and random ones, narrow and wide gates, 1..40 poses per call."""
+    for case in range(6):
+        n = int(rng.integers(5000, 40_001))
+        seed = int(rng.integers(1 << 30))
+        vol, qs = _few_orient_volume(np.random.default_rng(seed), n, k)
+        monkeypatch.setenv("DARE_ORIENT_SPLIT", "0")
+        canon, _ = _few_orient_volume(np.random.default_rng(seed), n, k)
+        _reslice_raw(canon, [ReslicePlane(Pose(Quaternion(1.0, 0.0, 0.0, 0.0), (5.0, 5.0, 5.0)), 4, 4,
+                                          (0.2, 0.2))], ResliceConfig(interp_radius=0.5), False)  # index decided
+        monkeypatch.delenv("DARE_ORIENT_SPLIT")
+        planes = []
+        for j in range(int(rng.choice([1, 2, 8, 40]))):
+            q = qs[j % k] + (rng.normal(scale=0.05, size=4) if j % 3 else rng.normal(size=4))
+            q /= np.linalg.norm(q)
+            planes.append(ReslicePlane(Pose(Quaternion(*q), rng.uniform(1, 9, 3)), 23, 19,
+                                       (float(rng.uniform(0.1, 0.4)),) * 2))
+        wide = bool(case % 2)
+        cfg = ResliceConfig(interp_radius=float(rng.uniform(0.25, 1.0)),
+                            normal_threshold_deg=float(rng.uniform(60, 89) if wide else rng.uniform(10, 40)),
+                            inplane_threshold_deg=float(rng.uniform(60, 89) if wide else rng.uniform(10, 40)),
+                            k_normal=float(rng.uniform(0, 20)), k_inplane=float(rng.uniform(0, 10)),
+                            k_dist=float(rng.choice([0.0, 2.0])), unassigned_value=int(rng.integers(0, 256)))
+        ex = _reslice_raw(vol, planes, cfg, True)
+        fa = _reslice_raw(vol, planes, cfg, False, 1)
+        ca = _reslice_raw(canon, planes, cfg, False, 1)
+        for got, what in ((fa, "split"), (ca, "canonical")):
+            np.testing.assert_array_equal(got[0], ex[0], err_msg=f"k {k} case {case} {what}")
+            np.testing.assert_array_equal(got[1], ex[1], err_msg=f"k {k} case {case} {what}")
+        p = planes[0]
+        ref = oracle.reslice(vol, oracle.plane_params(p), oracle.cfg_array(cfg), p.width, p.height,
+                             cfg.unassigned_value)
+        np.testing.assert_array_equal(fa[0][0], ref[0])
+        np.testing.assert_array_equal(fa[1][0], ref[1])
