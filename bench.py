@@ -853,7 +853,9 @@ def run_b200(args):
         main_kernel = f"reslice_k<{1 if (cfg.k_dist != 0 and _pow2(cfg.interp_radius)) else (2 if cfg.k_dist == 0 else 0)}>"
     else:
         n_or = int(info.n_orientations)
-        gmode = 2 if n_or == 1 else (1 if schedule == 1 and n_or <= 1024 else 0)  # register / smem / global gate
+        split = 2 <= n_or <= 1024 and schedule == 1 and os.environ.get("DARE_ORIENT_SPLIT") != "0"
+        # register / direction-cluster index (split.cu) / smem / global gate
+        gmode = 2 if n_or == 1 else (3 if split else (1 if schedule == 1 and n_or <= 1024 else 0))
         main_kernel = f"reslice_fast_k<{2 if cfg.k_dist == 0 else 0}, {gmode}, 1>"  # 1 part per pixel
     traffic, traffic_src = ncu_traffic(main_kernel, B, args.config)
     # launches per step: prep_k (gate table + launch order; gate_k alone when not sorted), main

@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdare_b200.so")
 LIB_CHECKED = os.path.join(HERE, "libdare_b200_checked.so")  # -DDARE_CHECKED: device bounds asserts
 SOURCES = ["runtime.cu", "reconstruct.cu", "volume_api.cu", "reslice.cu", "scalar.cu", "merge.cu", "bins.cu",
-           "plan.cu", "cells.cu", "similarity.cu"]
+           "plan.cu", "cells.cu", "similarity.cu", "split.cu"]
 HEADERS = ["common.cuh", "volume.cuh", "cells.cuh", "dare_exp.h", "exp_table.h"]
 
 

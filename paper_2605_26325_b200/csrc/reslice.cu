@@ -91,6 +91,13 @@ struct ResliceArgs {
   int inline_gate;
   const float4* orient;
   dare_reslice_cfg cfg;
+  // direction-cluster index (split.cu; kGateSplit launches): per cluster k the
+  // CSR s_offsets + k * ncells / s_bins + k * ncells over s_records
+  const uint32_t* s_offsets;
+  const uint32_t* s_bins;
+  const uint4* s_records;
+  const uint8_t* ocluster;  // orientation id -> cluster
+  int64_t ncells;
 };
 
 // gate table: one thread per (orientation, pose); the certified path's f32
@@ -440,6 +447,13 @@ struct FastWalk {
   // pmask: the column phases (p = 3 jx + jy) this thread walks -- all 9, or
   // with split pixels (small batches) those with p = part (mod 4).
   __device__ __forceinline__ bool open(const ResliceArgs& a, uint32_t& visits, uint32_t pmask = 0x1ffu) {
+    return open(a, -1, visits, pmask);
+  }
+  // the same over direction cluster k's CSR (kGateSplit; k < 0: the canonical one)
+  __device__ __forceinline__ bool open(const ResliceArgs& a, int k, uint32_t& visits, uint32_t pmask) {
+    const int64_t kbase = k < 0 ? 0 : (int64_t)k * a.ncells;
+    const uint32_t* __restrict__ offsets = (k < 0 ? a.offsets : a.s_offsets) + kbase;
+    const uint32_t* __restrict__ bins = (k < 0 ? a.bins : a.s_bins) + kbase;
     const int lox = xr & 0xffff, hix = (int)(xr >> 16) - 1, loy = yr & 0xffff, hiy = (int)(yr >> 16) - 1;
     const int loz = zr & 0xffff, hiz = (int)(zr >> 16) - 1;
     const int blo = (ph >> 4) & 3, bhi = (ph >> 6) & 3;
@@ -452,10 +466,10 @@ struct FastWalk {
           // last cell that lie wholly outside [zlo, zhi] (binned cells only)
           const int64_t base = ((int64_t)cx * a.dims[1] + cy) * a.dims[2];
           DARE_CHECK(cx >= 0 && cy >= 0 && loz >= 0 && base + hiz + 1 <= a.dims[0] * a.dims[1] * a.dims[2]);
-          const uint32_t o_lo = __ldg(a.offsets + base + loz);
-          const uint32_t o_hi = __ldg(a.offsets + base + hiz);
-          const uint32_t o_end = __ldg(a.offsets + base + hiz + 1);
-          const uint32_t w_lo = __ldg(a.bins + base + loz), w_hi = __ldg(a.bins + base + hiz);
+          const uint32_t o_lo = __ldg(offsets + base + loz);
+          const uint32_t o_hi = __ldg(offsets + base + hiz);
+          const uint32_t o_end = __ldg(offsets + base + hiz + 1);
+          const uint32_t w_lo = __ldg(bins + base + loz), w_hi = __ldg(bins + base + hiz);
           s = o_lo + ((w_lo >> 24) ? bin_start(w_lo, blo) : 0u);
           e = ((w_hi >> 24) && bhi < 3) ? o_hi + bin_start(w_hi, bhi + 1) : o_end;
           cy += 3;
@@ -496,7 +510,9 @@ struct FastWalk {
 // (pixel-major: the pose's row staged in shared memory), kGateSingle (volume
 // with one orientation id, e.g. linear sweeps with a fixed probe: the pose's
 // single gate value lives in a register and no lookup is made).
-constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2;
+// kGateSplit: kGateSmem over the direction-cluster index, walking only the
+// clusters that hold an orientation the pose accepts (split.cu).
+constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2, kGateSplit = 3;
 
 template <int kDistMode, int kGate>
 __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
@@ -634,12 +650,23 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     if (kGate == kGateSingle) g_single = sg[0];
   } else {
     if (kGate == kGateSingle) g_single = __ldg(gate);
-    if (kGate == kGateSmem) {  // pixel-major launch: one pose per block
+    if (kGate == kGateSmem || kGate == kGateSplit) {  // pixel-major launch: one pose per block
       float* sg = reinterpret_cast<float*>(smem_raw);
       for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) sg[i] = gate[i];
       __syncthreads();
       gate = sg;
     }
+  }
+  // direction clusters holding an orientation this pose accepts (kGateSplit)
+  uint32_t cmask = 0;
+  if constexpr (kGate == kGateSplit) {
+    __shared__ uint32_t s_cmask;
+    if (threadIdx.x == 0) s_cmask = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x)
+      if (gate[i] != CUDART_INF_F) atomicOr(&s_cmask, 1u << a.ocluster[i]);
+    __syncthreads();
+    cmask = s_cmask;
   }
   FastWalk w;
   float wh[3], wl[3];
@@ -686,7 +713,29 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   // single orientation gated out for this pose: no survivor anywhere (W = 0,
   // the pixel is certified uncovered without walking)
   if (kGate == kGateSingle && g_single == CUDART_INF_F) live = false;
-  if (live) live = w.open(a, visits, pmask);
+  if (kGate == kGateSplit && cmask == 0) live = false;
+  w.ph |= cmask << 8;  // (kGateSplit) clusters left to walk, lowest = current
+  // next non-empty column run: of the canonical CSR, or (kGateSplit) of the
+  // current cluster's CSR, moving to the next accepted cluster (column walk
+  // restarted) when one is exhausted
+  auto open_next = [&]() -> bool {
+    if constexpr (kGate != kGateSplit) {
+      return w.open(a, visits, pmask);
+    } else {
+      for (;;) {
+        const uint32_t left = w.ph >> 8;
+        if (w.open(a, __ffs(left) - 1, visits, pmask)) return true;
+        const uint32_t rest = left & (left - 1);
+        if (rest == 0) return false;
+        const int lox = w.xr & 0xffff, loy = w.yr & 0xffff;
+        const int jx = (int)(part / 3), jy = (int)(part % 3);
+        w.cur = (uint32_t)(lox + (jx - lox % 3 + 3) % 3) | ((uint32_t)(loy + (jy - loy % 3 + 3) % 3) << 16);
+        w.ph = (w.ph & 0xf0u) | (uint32_t)jx | ((uint32_t)jy << 2) | (rest << 8);
+      }
+    }
+  };
+  if (live) live = open_next();
+  const uint4* __restrict__ recs = kGate == kGateSplit ? a.s_records : a.records;
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
   // batches of 4 record slots = 2 aligned pairs (256-bit loads); slots outside
@@ -696,8 +745,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     uint4 r[4];
     const uint32_t last_pair = (w.e - 1) >> 1;
     DARE_CHECK(w.s < w.e && w.e <= a.n_samples && (i0 >> 1) <= last_pair);
-    load_pair(a.records, i0 >> 1, r[0], r[1]);
-    load_pair(a.records, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
+    load_pair(recs, i0 >> 1, r[0], r[1]);
+    load_pair(recs, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
     float bw = 0.0f, bj = 0.0f;
     // slot i is in the run iff i < e - i0 (and, for slot 0 only, i0 >= s: the
     // run starts at s or s - 1 rounded down to a pair)
@@ -705,13 +754,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     const bool first_ok = i0 >= w.s;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      fast_term<kDistMode, kGate>(r[i], (uint32_t)i < rem && (i > 0 || first_ok), w, gate, g_single, wh, wl,
-                                  c2, bw, bj);
+      fast_term<kDistMode, kGate == kGateSplit ? kGateSmem : kGate>(r[i], (uint32_t)i < rem && (i > 0 || first_ok),
+                                                                    w, gate, g_single, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
     i0 += 4;
     if (i0 >= w.e) {
-      live = w.open(a, visits, pmask);
+      live = open_next();
       i0 = w.s & ~1u;
     }
   }
@@ -1104,6 +1153,15 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   // the certified kernel's phased column walk shares loads better pixel-major
   // (cfg4: 16.8 vs 22.1 ms per 100 poses at 512^2)
   a.pose_major = (cfg->schedule == 2 || (cfg->schedule == 0 && coherent && !fast)) && !brute ? 1 : 0;
+  // multi-direction volumes: walk only the direction clusters a pose accepts
+  // (split.cu; built on the first certified launch)
+  const bool split = fast && !a.pose_major && vol->n_orient >= 2 && vol->n_orient <= kGateSmemF &&
+                     ensure_orient_split(vol, s);
+  a.s_offsets = split ? vol->d_soffsets : nullptr;
+  a.s_bins = split ? vol->d_sbins : nullptr;
+  a.s_records = split ? vol->d_srecords : nullptr;
+  a.ocluster = split ? vol->d_ocluster : nullptr;
+  a.ncells = vol->ncells;
   const bool sorted = P >= 4 && !brute && !a.pose_major;
   const uint64_t npix = (uint64_t)P * W * H;
   // ambiguity list: 1/16 of the launch's pixels (overflow -> exact recompute of all)
@@ -1171,9 +1229,11 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
       set_smem(reslice_fast_k<0, kGateGlobal, S>);
       set_smem(reslice_fast_k<0, kGateSmem, S>);
       set_smem(reslice_fast_k<0, kGateSingle, S>);
+      set_smem(reslice_fast_k<0, kGateSplit, S>);
       set_smem(reslice_fast_k<2, kGateGlobal, S>);
       set_smem(reslice_fast_k<2, kGateSmem, S>);
       set_smem(reslice_fast_k<2, kGateSingle, S>);
+      set_smem(reslice_fast_k<2, kGateSplit, S>);
     };
     reg(std::integral_constant<int, 1>{});
     reg(std::integral_constant<int, 2>{});
@@ -1192,7 +1252,8 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   }
   DARE_CUDA(cudaMemsetAsync(a.amb_count, 0, sizeof(unsigned), s));
   const int gmode = a.n_orient == 1 ? kGateSingle
-                                    : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal);
+                                    : (split ? kGateSplit
+                                             : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal));
   // small pixel-major batches: split pixels over 2 or 4 threads.  Cost model:
   // waves of resident warps x column phases per thread (9 / 5 / 3 for 1 / 2 /
   // 4 parts).  Measured at cfg2 (256x256 poses, us per launch, 1 / 2 / 4
@@ -1238,9 +1299,11 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
     constexpr int D = decltype(dm)::value;
     auto by_gate = [&](auto sp) {
       constexpr int S = decltype(sp)::value;
-      return gmode == kGateSingle ? reslice_fast_k<D, kGateSingle, S>
-                                  : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, S>
-                                                        : reslice_fast_k<D, kGateGlobal, S>);
+      return gmode == kGateSingle
+                 ? reslice_fast_k<D, kGateSingle, S>
+                 : (gmode == kGateSplit ? reslice_fast_k<D, kGateSplit, S>
+                                        : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, S>
+                                                              : reslice_fast_k<D, kGateGlobal, S>));
     };
     return parts == 4 ? by_gate(std::integral_constant<int, 4>{})
                       : (parts == 2 ? by_gate(std::integral_constant<int, 2>{})

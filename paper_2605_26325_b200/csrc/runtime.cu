@@ -302,6 +302,10 @@ dare_volume_s::~dare_volume_s() {
   dev_free(d_orient);
   dev_free(d_bins);
   dev_free(d_perm);
+  dev_free(d_soffsets);
+  dev_free(d_sbins);
+  dev_free(d_srecords);
+  dev_free(d_ocluster);
   cudaSetDevice(prev);
 }
 

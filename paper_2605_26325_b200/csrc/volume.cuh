@@ -24,6 +24,8 @@
 // the frame's quaternion (reconstruct.py:192-196), so oid = frame slot and the
 // per-pose orientation gates are evaluated once per oid, not per sample.
 #pragma once
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -42,6 +44,17 @@ struct dare_volume_s {
   float4* d_orient = nullptr;
   uint32_t* d_bins = nullptr;
   int8_t* d_perm = nullptr;
+  // Direction-cluster index for the certified reslice (split.cu, built on
+  // first use): the records again, grouped by the cluster of their beam
+  // direction (dominant axis of the sample normal and its sign: 6 clusters),
+  // one CSR per cluster over the same grid with the same z-quarter binning --
+  // a pose walks only the clusters holding an orientation its gate accepts.
+  uint32_t* d_soffsets = nullptr;  // n_clusters x ncells + 1 (cluster-major, absolute)
+  uint32_t* d_sbins = nullptr;     // n_clusters x ncells
+  uint4* d_srecords = nullptr;     // n_samples
+  uint8_t* d_ocluster = nullptr;   // n_orient: cluster of each orientation id
+  std::atomic<int> split_state{0};  // 0 not tried, 1 built, -1 not applicable
+  std::mutex split_mu;
   ~dare_volume_s();
 };
 
@@ -115,5 +128,9 @@ struct FrameSet {
   void wait_frames(cudaStream_t s, int64_t f_begin, int64_t f_end) const;
   ~FrameSet();
 };
+
+// Direction-cluster index (split.cu): builds it on first use if applicable;
+// true when vol->d_soffsets / d_sbins / d_srecords / d_ocluster are usable.
+bool ensure_orient_split(dare_volume_s* vol, cudaStream_t s);
 
 }  // namespace dare
