@@ -510,9 +510,10 @@ struct FastWalk {
 // (pixel-major: the pose's row staged in shared memory), kGateSingle (volume
 // with one orientation id, e.g. linear sweeps with a fixed probe: the pose's
 // single gate value lives in a register and no lookup is made).
-// kGateSplit: kGateSmem over the direction-cluster index, walking only the
-// clusters that hold an orientation the pose accepts (split.cu).
-constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2, kGateSplit = 3;
+// kGateSplit / kGateSplitG: kGateSmem / kGateGlobal over the direction-cluster
+// index, walking only the clusters that hold an orientation the pose accepts
+// (split.cu).
+constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2, kGateSplit = 3, kGateSplitG = 4;
 
 template <int kDistMode, int kGate>
 __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
@@ -635,7 +636,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   const uint32_t pmask = kParts == 4 ? (0x111u << part) & 0x1ffu : (kParts == 2 ? (0x155u << part) & 0x1ffu : 0x1ffu);
   const float* gate = a.gate2 + (size_t)pose * a.n_orient;
   float g_single = 0.0f;
-  if (kGate != kGateGlobal && kParts > 1 && a.inline_gate) {  // one pose per block: the row computed here
+  if (kGate != kGateGlobal && kGate != kGateSplitG && kParts > 1 && a.inline_gate) {  // the row computed here
     float* sg = reinterpret_cast<float*>(smem_raw);
     for (int i = threadIdx.x; i < a.n_orient; i += blockDim.x) {
       const double A = gate_value(a.orient, a.params, i, pose, a.cfg);
@@ -658,8 +659,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     }
   }
   // direction clusters holding an orientation this pose accepts (kGateSplit)
+  constexpr bool kSplitWalk = kGate == kGateSplit || kGate == kGateSplitG;
   uint32_t cmask = 0;
-  if constexpr (kGate == kGateSplit) {
+  if constexpr (kSplitWalk) {
     __shared__ uint32_t s_cmask;
     if (threadIdx.x == 0) s_cmask = 0;
     __syncthreads();
@@ -713,13 +715,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   // single orientation gated out for this pose: no survivor anywhere (W = 0,
   // the pixel is certified uncovered without walking)
   if (kGate == kGateSingle && g_single == CUDART_INF_F) live = false;
-  if (kGate == kGateSplit && cmask == 0) live = false;
+  if (kSplitWalk && cmask == 0) live = false;
   w.ph |= cmask << 8;  // (kGateSplit) clusters left to walk, lowest = current
   // next non-empty column run: of the canonical CSR, or (kGateSplit) of the
   // current cluster's CSR, moving to the next accepted cluster (column walk
   // restarted) when one is exhausted
   auto open_next = [&]() -> bool {
-    if constexpr (kGate != kGateSplit) {
+    if constexpr (!kSplitWalk) {
       return w.open(a, visits, pmask);
     } else {
       for (;;) {
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     }
   };
   if (live) live = open_next();
-  const uint4* __restrict__ recs = kGate == kGateSplit ? a.s_records : a.records;
+  const uint4* __restrict__ recs = kSplitWalk ? a.s_records : a.records;
   const float c2 = a.c2;
   double W = 0.0, J = 0.0;
   // batches of 4 record slots = 2 aligned pairs (256-bit loads); slots outside
@@ -754,7 +756,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
     const bool first_ok = i0 >= w.s;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      fast_term<kDistMode, kGate == kGateSplit ? kGateSmem : kGate>(r[i], (uint32_t)i < rem && (i > 0 || first_ok),
+      fast_term<kDistMode, kGate == kGateSplit ? kGateSmem : (kGate == kGateSplitG ? kGateGlobal : kGate)>(
+          r[i], (uint32_t)i < rem && (i > 0 || first_ok),
                                                                     w, gate, g_single, wh, wl, c2, bw, bj);
     W += (double)bw;
     J += (double)bj;
@@ -1155,8 +1158,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.pose_major = (cfg->schedule == 2 || (cfg->schedule == 0 && coherent && !fast)) && !brute ? 1 : 0;
   // multi-direction volumes: walk only the direction clusters a pose accepts
   // (split.cu; built on the first certified launch)
-  const bool split = fast && !a.pose_major && vol->n_orient >= 2 && vol->n_orient <= kGateSmemF &&
-                     ensure_orient_split(vol, s);
+  const bool split = fast && !a.pose_major && vol->n_orient >= 2 && ensure_orient_split(vol, s);
   a.s_offsets = split ? vol->d_soffsets : nullptr;
   a.s_bins = split ? vol->d_sbins : nullptr;
   a.s_records = split ? vol->d_srecords : nullptr;
@@ -1230,10 +1232,12 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
       set_smem(reslice_fast_k<0, kGateSmem, S>);
       set_smem(reslice_fast_k<0, kGateSingle, S>);
       set_smem(reslice_fast_k<0, kGateSplit, S>);
+      set_smem(reslice_fast_k<0, kGateSplitG, S>);
       set_smem(reslice_fast_k<2, kGateGlobal, S>);
       set_smem(reslice_fast_k<2, kGateSmem, S>);
       set_smem(reslice_fast_k<2, kGateSingle, S>);
       set_smem(reslice_fast_k<2, kGateSplit, S>);
+      set_smem(reslice_fast_k<2, kGateSplitG, S>);
     };
     reg(std::integral_constant<int, 1>{});
     reg(std::integral_constant<int, 2>{});
@@ -1252,7 +1256,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   }
   DARE_CUDA(cudaMemsetAsync(a.amb_count, 0, sizeof(unsigned), s));
   const int gmode = a.n_orient == 1 ? kGateSingle
-                                    : (split ? kGateSplit
+                                    : (split ? (a.n_orient <= kGateSmemF ? kGateSplit : kGateSplitG)
                                              : (!a.pose_major && a.n_orient <= kGateSmemF ? kGateSmem : kGateGlobal));
   // small pixel-major batches: split pixels over 2 or 4 threads.  Cost model:
   // waves of resident warps x column phases per thread (9 / 5 / 3 for 1 / 2 /
@@ -1301,9 +1305,11 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
       constexpr int S = decltype(sp)::value;
       return gmode == kGateSingle
                  ? reslice_fast_k<D, kGateSingle, S>
-                 : (gmode == kGateSplit ? reslice_fast_k<D, kGateSplit, S>
-                                        : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, S>
-                                                              : reslice_fast_k<D, kGateGlobal, S>));
+                 : (gmode == kGateSplit
+                        ? reslice_fast_k<D, kGateSplit, S>
+                        : (gmode == kGateSplitG ? reslice_fast_k<D, kGateSplitG, S>
+                                                : (gmode == kGateSmem ? reslice_fast_k<D, kGateSmem, S>
+                                                                      : reslice_fast_k<D, kGateGlobal, S>)));
     };
     return parts == 4 ? by_gate(std::integral_constant<int, 4>{})
                       : (parts == 2 ? by_gate(std::integral_constant<int, 2>{})

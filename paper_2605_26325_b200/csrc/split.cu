@@ -34,7 +34,7 @@ namespace dare {
 namespace {
 
 constexpr int kMaxClusters = 6;
-constexpr int64_t kMaxOrient = 1024;  // the certified kernel stages the pose's gate row in shared memory
+constexpr int64_t kMaxOrient = 1 << 20;  // (cluster ids: one byte per orientation)
 
 // Per cell and cluster: record count and the cluster run's z-quarter bins word.
 __global__ void split_count_k(int64_t ncells, const uint32_t* __restrict__ offsets,

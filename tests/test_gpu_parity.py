@@ -576,7 +576,7 @@ def test_split_pixel_variants_identical(rng, parts, monkeypatch):
 
 def _few_orient_volume(rng, n, k, extent=10.0, voxel=0.5):
     """Samples sharing k distinct orientations (sweeps at fixed probe
-    orientations), so the direction-cluster index applies (k <= 1024)."""
+    orientations; k > 1024 takes the global-gate form of the index walk)."""
     b = db.VolumeBuilder(db.BoundingBox((0, 0, 0), (extent,) * 3), voxel)
     qs = rng.normal(size=(k, 4))
     qs /= np.linalg.norm(qs, axis=1, keepdims=True)
@@ -586,7 +586,7 @@ def _few_orient_volume(rng, n, k, extent=10.0, voxel=0.5):
     return b.seal(), qs
 
 
-@pytest.mark.parametrize("k", [2, 3, 6, 17, 200])
+@pytest.mark.parametrize("k", [2, 3, 6, 17, 200, 2000])
 def test_direction_cluster_index_identical(rng, k, monkeypatch):
     """The certified path over the direction-cluster index (split.cu: only the
     clusters a pose accepts are walked) equals the exact FP64 path, the
