@@ -75,6 +75,9 @@ struct FrameView {
   // (group, cell); a (group, cell) with a single run gets its slot from the
   // per-group prefix table without an atomic
   uint32_t direct;
+  // fill cursors packed 4 per word (u8; one key CSR, every cell <= 255 samples):
+  // a quarter of the cursor footprint, so the cursor atomics stay in L2
+  uint32_t byte_cursors;
   const uint32_t* pre;  // (group, cell) -> samples of the cell in earlier groups | single-run << 31
   __device__ __forceinline__ size_t group_base(uint32_t chunk) const {
     return (size_t)(chunk / chunks_per_group) * ncells;
@@ -437,7 +440,14 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
       }
     }
     unsigned base = 0;
-    if (need && !solo && lane == leader) base = atomicAdd(&counts[lin], total);
+    if (need && !solo && lane == leader) {
+      if (fv.byte_cursors) {
+        const uint32_t sh = 8u * (lin & 3u);
+        base = (atomicAdd(&counts[lin >> 2], total << sh) >> sh) & 0xffu;
+      } else {
+        base = atomicAdd(&counts[lin], total);
+      }
+    }
     base = __shfl_sync(0xffffffffu, base, leader);
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
@@ -941,7 +951,7 @@ __global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict
 // `scatter(fill, counts, offsets, keys, rejected)` launches the source's pass.
 template <class Rec, class Scatter>
 void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int seal_carveout = -1,
-               uint32_t groups = 1, uint32_t* direct_pre = nullptr) {
+               uint32_t groups = 1, uint32_t* direct_pre = nullptr, bool byte_ok = false) {
   const int64_t ncells = vol->ncells;
   const int64_t nkc = ncells * (int64_t)groups;  // per-group counters (groups > 1: frame-grouped keys)
   DARE_LIMIT(nkc < (int64_t)UINT32_MAX, "too many cells x frame groups");
@@ -957,7 +967,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   Scratch<uint32_t> totals(groups > 1 ? ncells + 1 : 0, s);
   pt.mark("alloc+memset");
   using Key = typename Rec::Key;
-  scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr);
+  scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr, false);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
   size_t tmp_bytes = 0, max_bytes = 0, tmp2_bytes = 0;
@@ -1004,11 +1014,14 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     return;
   }
   Scratch<Key> keys(n_kept + 4, s);  // + slack: the seal's 16 B-aligned bulk copies may read past the end
-  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * nkc, s));
+  // one key CSR and no cell over 255 samples: u8 fill cursors, 4 per word
+  const char* u8_env = getenv("DARE_FILL_U8");
+  const bool byte_cursors = byte_ok && groups == 1 && !direct && max_run <= 255 && !(u8_env && u8_env[0] == '0');
+  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, byte_cursors ? 4 * ((size_t)ncells / 4 + 1) : sizeof(uint32_t) * nkc, s));
   pt.mark("readback+alloc");
   if (groups > 1 && !direct) {
     Scratch<Key> gkeys(n_kept, s);
-    scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr);
+    scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr, false);
     DARE_CUDA(cudaGetLastError());
     pt.mark("fill");
     regroup_keys_k<Key><<<ceil_div(ceil_div(ncells, 32) * 32, 256), 256, 0, s>>>(
@@ -1016,7 +1029,8 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     DARE_CUDA(cudaGetLastError());
     pt.mark("regroup");
   } else {
-    scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr, (unsigned long long*)nullptr);
+    scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr, (unsigned long long*)nullptr,
+            byte_cursors);
     DARE_CUDA(cudaGetLastError());
     pt.mark("fill");
   }
@@ -1118,7 +1132,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
                  (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
                  FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw,
-                 0xffffffffu, (uint32_t)vol->ncells, 0u, nullptr};
+                 0xffffffffu, (uint32_t)vol->ncells, 0u, 0u, nullptr};
     {
       const uint32_t ub = ceil_log2((uint64_t)width), vb = ceil_log2((uint64_t)height);
       if (ub + vb + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 32 && ub + vb < 32) {
@@ -1154,8 +1168,9 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                              narrow_env && narrow_env[0] == '1';
     const bool narrow = narrow_keys;
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
-                       unsigned long long* rej) {
+                       unsigned long long* rej, bool byte_cursors) {
       if (n_frames == 0) return;
+      fv.byte_cursors = byte_cursors ? 1u : 0u;
       if (!fill) {  // needs no intensities: runs while host frames are still uploading
         if (tabs_ok)
           frame_count_tab_k<true><<<dim3(tiles, chunks), 256, 0, s>>>(fv, ct, m, counts, runs.ptr, nruns.ptr, rej);
@@ -1219,9 +1234,11 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
       }
     }
     if (narrow_keys)
-      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr);
+      build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr,
+                true);
     else
-      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr);
+      build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr,
+                true);
     clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
@@ -1261,7 +1278,7 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
     const float* pos = d_pos.ptr;
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
-                       unsigned long long* rej) {
+                       unsigned long long* rej, bool) {
       if (n_samples == 0) return;
       if (fill)
         sample_scatter_k<true><<<ceil_div(n_samples, 256), 256, 0, s>>>(

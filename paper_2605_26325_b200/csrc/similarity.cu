@@ -486,14 +486,17 @@ void launch_similarity(int32_t P, int32_t H, int32_t W, const T* a, const uint8_
   Scratch<double> scr((size_t)chunk * per_pair, s);
   Scratch<double> vals((size_t)chunk * WN, s);
   Scratch<uint8_t> flags((size_t)chunk * WN, s);
-  const int nt = kU8 ? 128 : (win <= 31 ? 128 : 32);
-  const size_t smem = kU8 ? (((size_t)(win + 1) * 3 * (nt + win - 1) + 15) & ~(size_t)15) +
-                                (size_t)(win + 1) * 6 * nt * sizeof(int)
-                          : ((size_t)win * 6 * nt + 3 * (size_t)(nt + win - 1)) * sizeof(double);
+  // u8 images up to 31-wide windows: integer running sums (ssim_window_u8_k);
+  // otherwise the f64 ring kernel (integer-valued inputs give the same sums)
+  const bool u8_kernel = kU8 && win <= 31;
+  const int nt = u8_kernel || win <= 31 ? 128 : 32;
+  const size_t smem = u8_kernel ? (((size_t)(win + 1) * 3 * (nt + win - 1) + 15) & ~(size_t)15) +
+                                      (size_t)(win + 1) * 6 * nt * sizeof(int)
+                                : ((size_t)win * 6 * nt + 3 * (size_t)(nt + win - 1)) * sizeof(double);
   using WindowFn = void (*)(const T*, const uint8_t*, const T*, const uint8_t*, int, int, int, double, double,
                             double*, uint8_t*);
-  auto window_kernel = kU8 ? (win == 7 ? (WindowFn)ssim_window_u8_k<7> : (WindowFn)ssim_window_u8_k<0>)
-                           : ssim_window_k<T>;
+  auto window_kernel = u8_kernel ? (win == 7 ? (WindowFn)ssim_window_u8_k<7> : (WindowFn)ssim_window_u8_k<0>)
+                                 : ssim_window_k<T>;
   if (do_ssim) {
     DARE_LIMIT(smem <= 220 * 1024 && win <= 127, "ssim window too large (at most 127)");
     DARE_CUDA(cudaFuncSetAttribute((const void*)window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

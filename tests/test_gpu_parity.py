@@ -64,7 +64,7 @@ def _random_sweep(rng, n, h, w, pitch, spread):
 @pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
                                        ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7"), ("DARE_KEY_MODE", "0"),
                                        ("DARE_COMPOUND_TABLES", "1"), ("DARE_COMPOUND_V1", "1"),
-                                       ("DARE_SEAL_BULK", "1")])
+                                       ("DARE_SEAL_BULK", "1"), ("DARE_FILL_U8", "0")])
 @pytest.mark.parametrize("key", REC_KEYS)
 def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
@@ -134,15 +134,16 @@ def test_reconstruct_host_frames_many_upload_groups():
     assert_volume_equal(v, ref)
 
 
-def test_reconstruct_dense_cells_use_large_run_path():
-    # many frames at one pose: > 32 samples per cell -> segmented-sort path
+@pytest.mark.parametrize("n", [8, 80])
+def test_reconstruct_dense_cells_use_large_run_path(n):
+    # many frames at one pose: > 32 samples per cell -> segmented-sort path;
+    # n = 8 keeps every cell <= 255 samples (u8 fill cursors), n = 80 does not
     rng = np.random.default_rng(5)
-    n = 80
     ts = np.arange(n) * 0.1
     rec = db.SweepRecording(rng.integers(0, 256, (n, 6, 5), dtype=np.uint8), ts, ts, [Pose.identity()] * n,
                             (0.05, 0.05))
     v = db.reconstruct_volume(rec, voxel_size=0.5, margin=0.25)
-    assert v.cell_counts.max() > 32
+    assert v.cell_counts.max() > 32 and (v.cell_counts.max() <= 255) == (n == 8)
     assert_volume_equal(v, oracle.reconstruct(rec, 0.5, 0.25))
 
 
