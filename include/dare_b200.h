@@ -91,7 +91,8 @@ typedef struct {
                                      of cells stored grouped by z quarter, 0 otherwise */
   const int8_t* d_perm;           /* n_samples: the cell's j-th sample in insertion order
                                      (index J = offsets[c] + j) is stored at J + perm[J] */
-  size_t device_bytes;
+  size_t device_bytes;  /* all buffers of the handle, incl. the direction-cluster index of a
+                           multi-direction volume once the first certified reslice built it */
 } dare_volume_info;
 
 typedef struct {

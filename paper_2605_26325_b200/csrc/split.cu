@@ -170,6 +170,7 @@ bool ensure_orient_split(dare_volume_s* vol, cudaStream_t s) {
   vol->d_soffsets = d_soff;
   vol->d_sbins = d_sbins;
   vol->d_srecords = d_srec;
+  vol->split_bytes = need + clu.size();
   vol->split_state = 1;
   return true;
 }

@@ -54,6 +54,7 @@ struct dare_volume_s {
   uint4* d_srecords = nullptr;     // n_samples
   uint8_t* d_ocluster = nullptr;   // n_orient: cluster of each orientation id
   std::atomic<int> split_state{0};  // 0 not tried, 1 built, -1 not applicable
+  size_t split_bytes = 0;           // device bytes of the index once built
   std::mutex split_mu;
   ~dare_volume_s();
 };

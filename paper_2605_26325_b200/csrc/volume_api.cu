@@ -297,7 +297,7 @@ extern "C" int dare_volume_get_info(dare_volume_t vol, dare_volume_info* info) {
     info->d_bins = vol->d_bins;
     info->d_perm = vol->d_perm;
     info->device_bytes = sizeof(uint32_t) * (2 * vol->ncells + 1) + (sizeof(uint4) + 1) * vol->n_samples +
-                         sizeof(float4) * vol->n_orient;
+                         sizeof(float4) * vol->n_orient + (vol->split_state > 0 ? vol->split_bytes : 0);
   });
 }
 
