@@ -78,6 +78,10 @@ struct FrameView {
   // fill cursors packed 4 per word (u8; one key CSR, every cell <= 255 samples):
   // a quarter of the cursor footprint, so the cursor atomics stay in L2
   uint32_t byte_cursors;
+  // bucketed fill (64-bit keys): slots per bucket of kBucketCells cells, the
+  // key tagged with its cell within the bucket; bucket_place_k then places the
+  // bucket's keys in their cells through shared memory (see build_csr)
+  uint32_t bucketed;
   const uint32_t* pre;  // (group, cell) -> samples of the cell in earlier groups | single-run << 31
   __device__ __forceinline__ size_t group_base(uint32_t chunk) const {
     return (size_t)(chunk / chunks_per_group) * ncells;
@@ -168,6 +172,10 @@ constexpr int kMaxRun = 8;  // bins of a run's samples fit 16 bits
 // the seal need not recompute z; it sits below the index, so key order is
 // insertion order.
 constexpr int kKeyShift = 10;
+// bucketed fill: 1024 cells per bucket, the cell within the bucket in key bits
+// 42.. (insertion index << kKeyShift | bin << 8 | byte uses bits 0..41)
+constexpr int kBucketShift = 10, kBucketCells = 1 << kBucketShift, kBucketTag = 42;
+constexpr int kPlaceCap = 24 * 1024;  // keys of one bucket staged in shared memory (192 KB)
 
 
 template <bool kInv>
@@ -418,9 +426,12 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     uint32_t pre_w = 0;
     if (fv.direct && need) pre_w = fv.pre[gb + lin];
     const bool solo = (pre_w >> 31) != 0;  // the only run of its (group, cell): slot known, no atomic
-    const uint32_t cell_off = need ? offsets[lin] + (pre_w & 0x7fffffffu) : 0u;  // early: overlaps the atomic
+    // bucketed: slots per bucket (absolute cursors), grouping by bucket
+    const bool bk = kWide && fv.bucketed;
+    const uint32_t gkey = bk ? lin >> kBucketShift : lin;
+    const uint32_t cell_off = (need && !bk) ? offsets[lin] + (pre_w & 0x7fffffffu) : 0u;  // early: overlaps the atomic
     // lanes not emitting (or solo) get a key no cell has, so MATCH runs on the full warp
-    const unsigned peers = __match_any_sync(0xffffffffu, (need && !solo) ? lin : (0x80000000u | lane));
+    const unsigned peers = __match_any_sync(0xffffffffu, (need && !solo) ? gkey : (0x80000000u | lane));
     // Groups whose runs cover the same frames (the common case: image
     // neighbours crossing a cell together) take their slots frame-major --
     // (frame, pixel) = insertion order -- so the seal's sort finds them presorted.
@@ -441,7 +452,9 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     }
     unsigned base = 0;
     if (need && !solo && lane == leader) {
-      if (fv.byte_cursors) {
+      if (bk) {
+        base = atomicAdd(&counts[gkey], total);
+      } else if (fv.byte_cursors) {
         const uint32_t sh = 8u * (lin & 3u);
         base = (atomicAdd(&counts[lin >> 2], total << sh) >> sh) & 0xffu;
       } else {
@@ -452,10 +465,12 @@ __global__ void __launch_bounds__(256) frame_fill_k(FrameView fv, uint32_t chunk
     if (need) {
       const unsigned n = __popc(peers), rank = __popc(peers & lt);
       const uint32_t stride = uniform ? n : 1u;
-      DARE_CHECK(fv.direct || base + total <= offsets[lin + 1] - cell_off);
+      DARE_CHECK(fv.direct || bk || base + total <= offsets[lin + 1] - cell_off);
+      DARE_CHECK(!bk || base + total <= offsets[min((gkey + 1) << kBucketShift, fv.ncells)]);
       Key* dst = keys + cell_off + base + (uniform ? rank : prefix);
       if constexpr (kWide) {
-        const unsigned long long key0 = ((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift;
+        const unsigned long long key0 = (((unsigned long long)((f0 + run_j) * fv.fstride + pk)) << kKeyShift) |
+                                        (bk ? (unsigned long long)(lin & (kBucketCells - 1)) << kBucketTag : 0ull);
         const unsigned long long kstep = (unsigned long long)fv.fstride << kKeyShift;
 #pragma unroll
         for (int t = 0; t < kMaxRun; ++t) {
@@ -947,11 +962,59 @@ __global__ void __launch_bounds__(256) regroup_keys_k(const uint32_t* __restrict
   }
 }
 
+// Bucketed fill, placement: CTA per bucket of kBucketCells cells.  The bucket's
+// keys (tagged with their cell within the bucket) occupy exactly the bucket's
+// key range; they are placed into their cells through shared memory and the
+// range is written back in place, coalesced -- no partially written 32 B
+// sectors reach DRAM, unlike a fill that scatters each run straight into its
+// cell (cfg3: one lone pixel per cell and sweep).
+__global__ void __launch_bounds__(1024) bucket_place_k(const uint32_t* __restrict__ offsets, int64_t ncells,
+                                                       unsigned long long* keys) {
+  extern __shared__ unsigned long long sreg[];  // kPlaceCap
+  __shared__ uint32_t scur[kBucketCells];
+  const int64_t c0 = (int64_t)blockIdx.x << kBucketShift;
+  const int64_t c1 = min(c0 + (int64_t)kBucketCells, ncells);
+  const uint32_t r0 = offsets[c0], n = offsets[c1] - r0;
+  DARE_CHECK(n <= (uint32_t)kPlaceCap);
+  for (int c = threadIdx.x; c < kBucketCells; c += blockDim.x) scur[c] = c0 + c < c1 ? offsets[c0 + c] - r0 : 0u;
+  __syncthreads();
+  // four loads in flight per thread, then their placements
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+    unsigned long long e[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = i0 + q * blockDim.x;
+      e[q] = i < n ? __ldcs(keys + r0 + i) : ~0ull;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (e[q] != ~0ull) {
+        const uint32_t slot = atomicAdd(&scur[(uint32_t)(e[q] >> kBucketTag)], 1u);
+        DARE_CHECK(slot < n);
+        sreg[slot] = e[q] & ((1ull << kBucketTag) - 1ull);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[r0 + i] = sreg[i];
+}
+
+// Bucket cursors (the key offset of each bucket's first cell) and the largest bucket.
+__global__ void bucket_init_k(const uint32_t* __restrict__ offsets, int64_t ncells, int64_t nb, uint32_t* cursors,
+                              uint32_t* max_bucket) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int64_t c0 = b << kBucketShift, c1 = min(c0 + (int64_t)kBucketCells, ncells);
+  cursors[b] = offsets[c0];
+  atomicMax(max_bucket, offsets[c1] - offsets[c0]);
+}
+
 // count -> scan -> fill -> seal, shared by frames and arbitrary samples.
 // `scatter(fill, counts, offsets, keys, rejected)` launches the source's pass.
 template <class Rec, class Scatter>
 void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int seal_carveout = -1,
-               uint32_t groups = 1, uint32_t* direct_pre = nullptr, bool byte_ok = false) {
+               uint32_t groups = 1, uint32_t* direct_pre = nullptr, bool byte_ok = false,
+               bool bucket_ok = false) {
   const int64_t ncells = vol->ncells;
   const int64_t nkc = ncells * (int64_t)groups;  // per-group counters (groups > 1: frame-grouped keys)
   DARE_LIMIT(nkc < (int64_t)UINT32_MAX, "too many cells x frame groups");
@@ -967,7 +1030,7 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   Scratch<uint32_t> totals(groups > 1 ? ncells + 1 : 0, s);
   pt.mark("alloc+memset");
   using Key = typename Rec::Key;
-  scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr, false);
+  scatter(false, counts.ptr, (const uint32_t*)nullptr, (void*)nullptr, rej.ptr, false, false);
   DARE_CUDA(cudaGetLastError());
   pt.mark("count");
   size_t tmp_bytes = 0, max_bytes = 0, tmp2_bytes = 0;
@@ -1016,12 +1079,28 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
   Scratch<Key> keys(n_kept + 4, s);  // + slack: the seal's 16 B-aligned bulk copies may read past the end
   // one key CSR and no cell over 255 samples: u8 fill cursors, 4 per word
   const char* u8_env = getenv("DARE_FILL_U8");
-  const bool byte_cursors = byte_ok && groups == 1 && !direct && max_run <= 255 && !(u8_env && u8_env[0] == '0');
-  DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, byte_cursors ? 4 * ((size_t)ncells / 4 + 1) : sizeof(uint32_t) * nkc, s));
+  bool byte_cursors = byte_ok && groups == 1 && !direct && max_run <= 255 && !(u8_env && u8_env[0] == '0');
+  // bucketed fill (frames whose pixels rarely share a cell, e.g. pitch >= voxel:
+  // every run is a lone scattered write): if every bucket fits the placement stage
+  bool bucketed = bucket_ok && groups == 1 && !direct && sizeof(Key) == 8;
+  const int64_t nb = (ncells + kBucketCells - 1) >> kBucketShift;
+  if (bucketed) {
+    Scratch<uint32_t> maxb(1, s);
+    DARE_CUDA(cudaMemsetAsync(maxb.ptr, 0, sizeof(uint32_t), s));
+    bucket_init_k<<<ceil_div(nb, 256), 256, 0, s>>>(vol->d_offsets, ncells, nb, counts.ptr, maxb.ptr);
+    DARE_CUDA(cudaGetLastError());
+    uint32_t h_maxb = 0;
+    DARE_CUDA(cudaMemcpyAsync(&h_maxb, maxb.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    DARE_CUDA(cudaStreamSynchronize(s));
+    bucketed = h_maxb <= (uint32_t)kPlaceCap;
+    byte_cursors = false;
+  }
+  if (!bucketed)
+    DARE_CUDA(cudaMemsetAsync(counts.ptr, 0, byte_cursors ? 4 * ((size_t)ncells / 4 + 1) : sizeof(uint32_t) * nkc, s));
   pt.mark("readback+alloc");
   if (groups > 1 && !direct) {
     Scratch<Key> gkeys(n_kept, s);
-    scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr, false);
+    scatter(true, counts.ptr, (const uint32_t*)koff.ptr, (void*)gkeys.ptr, (unsigned long long*)nullptr, false, false);
     DARE_CUDA(cudaGetLastError());
     pt.mark("fill");
     regroup_keys_k<Key><<<ceil_div(ceil_div(ncells, 32) * 32, 256), 256, 0, s>>>(
@@ -1030,9 +1109,20 @@ void build_csr(dare_volume_s* vol, Rec rec, Scatter scatter, cudaStream_t s, int
     pt.mark("regroup");
   } else {
     scatter(true, counts.ptr, (const uint32_t*)vol->d_offsets, (void*)keys.ptr, (unsigned long long*)nullptr,
-            byte_cursors);
+            byte_cursors, bucketed);
     DARE_CUDA(cudaGetLastError());
     pt.mark("fill");
+    if (bucketed) {
+      static std::once_flag place_attr;
+      std::call_once(place_attr, [] {
+        DARE_CUDA(cudaFuncSetAttribute(bucket_place_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(unsigned long long) * kPlaceCap)));
+      });
+      bucket_place_k<<<(unsigned)nb, 1024, sizeof(unsigned long long) * kPlaceCap, s>>>(
+          vol->d_offsets, ncells, (unsigned long long*)keys.ptr);
+      DARE_CUDA(cudaGetLastError());
+      pt.mark("place");
+    }
   }
   uint32_t* big_cells = counts.ptr;  // reuse: #big runs <= ncells
   Scratch<uint32_t> n_big_d(1, s);
@@ -1132,7 +1222,7 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
     FrameView fv{fs.d_frames, fs.d_image, fs.d_axes, fs.d_mask, (uint32_t)n_frames,
                  (uint32_t)height, (uint32_t)width, (uint32_t)hw, pitch_x, pitch_y, d_oid.ptr,
                  FastDiv((uint32_t)width), FastDiv((uint32_t)hw), 0u, 0u, 0u, (uint32_t)hw,
-                 0xffffffffu, (uint32_t)vol->ncells, 0u, 0u, nullptr};
+                 0xffffffffu, (uint32_t)vol->ncells, 0u, 0u, 0u, nullptr};
     {
       const uint32_t ub = ceil_log2((uint64_t)width), vb = ceil_log2((uint64_t)height);
       if (ub + vb + ceil_log2((uint64_t)std::max<int64_t>(n_frames, 1)) <= 32 && ub + vb < 32) {
@@ -1168,9 +1258,10 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
                              narrow_env && narrow_env[0] == '1';
     const bool narrow = narrow_keys;
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
-                       unsigned long long* rej, bool byte_cursors) {
+                       unsigned long long* rej, bool byte_cursors, bool bucketed) {
       if (n_frames == 0) return;
       fv.byte_cursors = byte_cursors ? 1u : 0u;
+      fv.bucketed = bucketed ? 1u : 0u;
       if (!fill) {  // needs no intensities: runs while host frames are still uploading
         if (tabs_ok)
           frame_count_tab_k<true><<<dim3(tiles, chunks), 256, 0, s>>>(fv, ct, m, counts, runs.ptr, nruns.ptr, rej);
@@ -1233,12 +1324,17 @@ extern "C" int dare_reconstruct(const uint8_t* frames, int64_t n_images, int32_t
         }
       }
     }
+    // bucketed fill when image neighbours rarely share a cell (pixel pitch >= ~3/4 voxel:
+    // the fill's MATCH finds no lane to aggregate with and every run is a lone
+    // scattered write); DARE_FILL_BUCKETS=1 / 0 forces it on / off
+    const char* bk_env = getenv("DARE_FILL_BUCKETS");
+    const bool bucket_ok = bk_env ? bk_env[0] == '1' : std::min(pitch_x, pitch_y) >= 0.75 * voxel_size;
     if (narrow_keys)
       build_csr(vol.get(), FrameRecords32{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr,
                 true);
     else
       build_csr(vol.get(), FrameRecords{fv, sa.ptr}, scatter, s, carve, groups, fv.direct ? pre_store.ptr : nullptr,
-                true);
+                true, bucket_ok);
     clock.stop();
     DARE_CUDA(cudaStreamSynchronize(s));
     if (rejected_out_of_bounds) *rejected_out_of_bounds = vol->rejected;
@@ -1278,7 +1374,7 @@ extern "C" int dare_volume_seal(const double* origin, double voxel_size, const i
     VoxelMap m = make_voxel_map(origin, voxel_size, dims);
     const float* pos = d_pos.ptr;
     auto scatter = [&](bool fill, uint32_t* counts, const uint32_t* offsets, void* keys,
-                       unsigned long long* rej, bool) {
+                       unsigned long long* rej, bool, bool) {
       if (n_samples == 0) return;
       if (fill)
         sample_scatter_k<true><<<ceil_div(n_samples, 256), 256, 0, s>>>(

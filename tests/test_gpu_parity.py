@@ -64,7 +64,8 @@ def _random_sweep(rng, n, h, w, pitch, spread):
 @pytest.mark.parametrize("env,value", [("DARE_COUNT_LEGACY", "1"), ("DARE_NARROW_KEYS", "1"),
                                        ("DARE_KEY_GROUPS", "3"), ("DARE_KEY_GROUPS", "7"), ("DARE_KEY_MODE", "0"),
                                        ("DARE_COMPOUND_TABLES", "1"), ("DARE_COMPOUND_V1", "1"),
-                                       ("DARE_SEAL_BULK", "1"), ("DARE_FILL_U8", "0")])
+                                       ("DARE_SEAL_BULK", "1"), ("DARE_FILL_U8", "0"), ("DARE_FILL_BUCKETS", "1"),
+                                       ("DARE_FILL_BUCKETS", "0")])
 @pytest.mark.parametrize("key", REC_KEYS)
 def test_reconstruct_alternative_passes_match_reference(golden, key, env, value, monkeypatch):
     """The kept alternative passes (the FP64-chain count / compound kernels used
@@ -626,3 +627,19 @@ def test_direction_cluster_index_identical(rng, k, monkeypatch):
                              cfg.unassigned_value)
         np.testing.assert_array_equal(fa[0][0], ref[0])
         np.testing.assert_array_equal(fa[1][0], ref[1])
+
+
+@pytest.mark.parametrize("n", [8, 1000])
+def test_bucketed_fill_forced_and_oversized_buckets(n, monkeypatch):
+    """DARE_FILL_BUCKETS=1: the bucketed fill on a dense stack (n = 8: every
+    bucket fits the placement stage) and with a bucket over its capacity
+    (n = 1000: 30k samples in one cell -> the per-cell fill), both equal to the
+    oracle."""
+    monkeypatch.setenv("DARE_FILL_BUCKETS", "1")
+    rng = np.random.default_rng(7)
+    ts = np.arange(n) * 0.1
+    rec = db.SweepRecording(rng.integers(0, 256, (n, 6, 5), dtype=np.uint8), ts, ts, [Pose.identity()] * n,
+                            (0.05, 0.05))
+    v = db.reconstruct_volume(rec, voxel_size=0.5, margin=0.25)
+    assert (v.cell_counts.max() > 24 * 1024) == (n == 1000)
+    assert_volume_equal(v, oracle.reconstruct(rec, 0.5, 0.25))
