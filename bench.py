@@ -660,8 +660,14 @@ def run_b200(args):
     if ws > 1:
         import torch.distributed as dist
 
+        import datetime
+
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # failure detection: the NCCL watchdog aborts a collective stuck for 10 min
+        # (a dead or hung rank) instead of hanging the job
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "3")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=10))
 
     def barrier():
         if dist is not None:
