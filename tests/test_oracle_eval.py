@@ -104,3 +104,36 @@ def test_report_files(tmp_path, monkeypatch):
     assert lines[0] == "id,method,ncc,ssim,latency_ms" and len(lines) == 13
     txt = open(paths["txt"]).read()
     assert txt.startswith("paired comparison: dare vs baseline (6 pairs)") and "latency[dare]" in txt
+
+
+def test_run_comparison_contract(monkeypatch):
+    """Exclusions on either side, pair ids zipped with the images (the
+    reference's zip semantics), every pair undefined -> InvalidArgumentError,
+    timing statistics from latencies."""
+    from paper_2605_26325_b200.reslice import ResliceImage
+
+    img = ResliceImage(pixels=np.zeros((8, 8), np.uint8), coverage=np.ones((8, 8), bool), timing_ms=0.0)
+    n = 7
+
+    def fake(cands, truths):
+        out = []
+        for k in range(len(cands)):
+            side, pair = divmod(k, n)
+            if (pair == 2 and side == 0) or (pair == 5 and side == 1):
+                out.append(ev.UndefinedMetricError(f"undefined {side} {pair}"))
+            else:
+                out.append(ev.SimilarityResult(0.5 + 0.01 * pair * (1 - side), 0.4 + 0.02 * pair * (1 - side), 64))
+        return out
+
+    monkeypatch.setattr(ev, "compare_images_batch", fake)
+    rep = ev.run_comparison([img] * n, [img] * n, [img] * n, latencies={"dare": [1.0, 3.0], "baseline": []})
+    assert rep.pair_ids == ["pair0000", "pair0001", "pair0003", "pair0004", "pair0006"]
+    assert [e["reason"] for e in rep.summary["excluded_pairs"]] == ["undefined 0 2", "undefined 1 5"]
+    assert rep.timing == {"dare": ev.latency_stats([1.0, 3.0])}
+    rep2 = ev.run_comparison([img] * n, [img] * n, [img] * n, pair_ids=["a", "b", "c"])
+    assert rep2.pair_ids == ["a", "b"] and rep2.summary["pair_count"] == 2  # 'c' is pair 2: excluded
+    monkeypatch.setattr(ev, "compare_images_batch", lambda c, t: [ev.UndefinedMetricError("x")] * len(c))
+    with pytest.raises(InvalidArgumentError, match="every pair had undefined metrics"):
+        ev.run_comparison([img] * 3, [img] * 3, [img] * 3)
+    with pytest.raises(InvalidArgumentError, match="equal-length non-empty"):
+        ev.run_comparison([], [], [])
