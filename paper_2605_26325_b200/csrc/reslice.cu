@@ -98,6 +98,7 @@ struct ResliceArgs {
   const uint4* s_records;
   const uint8_t* ocluster;  // orientation id -> cluster
   int64_t ncells;
+  int csingle[6];  // per cluster: its orientation id when it holds exactly one, else -1
 };
 
 // gate table: one thread per (orientation, pose); the certified path's f32
@@ -513,17 +514,19 @@ struct FastWalk {
 // kGateSplit / kGateSplitG: kGateSmem / kGateGlobal over the direction-cluster
 // index, walking only the clusters that hold an orientation the pose accepts
 // (split.cu).
-constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2, kGateSplit = 3, kGateSplitG = 4;
+// kGateUniform (record term only): one gate value in a register for every
+// record walked, which may carry any orientation id (a one-orientation cluster).
+constexpr int kGateGlobal = 0, kGateSmem = 1, kGateSingle = 2, kGateSplit = 3, kGateSplitG = 4, kGateUniform = 5;
 
 template <int kDistMode, int kGate>
 __device__ __forceinline__ void fast_term(const uint4& c, bool valid, const FastWalk& w,
                                           const float* gate, float g_single, const float (&wh)[3],
                                           const float (&wl)[3], float c2, float& bw, float& bj) {
-  DARE_CHECK(!valid || kGate == kGateSingle || (c.w >> 8) < 1024u || kGate == kGateGlobal);
-  const float g = kGate == kGateSingle ? g_single
-                                       : (kGate == kGateSmem ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8)));
-  // (single orientation: a gated-out pose never walks, see reslice_fast_k)
-  const bool k = valid && w.in_cube(c) && (kGate == kGateSingle || g != CUDART_INF_F);
+  constexpr bool kReg = kGate == kGateSingle || kGate == kGateUniform;  // gate value in a register
+  DARE_CHECK(!valid || kReg || (c.w >> 8) < 1024u || kGate == kGateGlobal);
+  const float g = kReg ? g_single : (kGate == kGateSmem ? gate[c.w >> 8] : __ldg(gate + (c.w >> 8)));
+  // (register gate: a gated-out pose / cluster is never walked, see reslice_fast_k)
+  const bool k = valid && w.in_cube(c) && (kReg || g != CUDART_INF_F);
   float arg = g;
   if (kDistMode != 2) {
     // (x, y) as one f32x2 lane pair (FADD2 / FMUL2); same roundings as scalar
@@ -669,7 +672,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
       if (gate[i] != CUDART_INF_F) atomicOr(&s_cmask, 1u << a.ocluster[i]);
     __syncthreads();
     cmask = s_cmask;
+    // one accepted cluster holding one orientation (e.g. a pose aligned with one
+    // of several sweeps): every walked record has that orientation -> register gate
+    if (__popc(cmask) == 1) {
+      const int o = a.csingle[__ffs(cmask) - 1];
+      if (o >= 0) g_single = gate[o];
+    }
   }
+  const bool uni = kSplitWalk && __popc(cmask) == 1 && a.csingle[__ffs(cmask) - 1] >= 0;
   FastWalk w;
   float wh[3], wl[3];
   bool live;
@@ -743,29 +753,39 @@ __global__ void __launch_bounds__(kFastThreads, kFastBlocks) reslice_fast_k(Resl
   // batches of 4 record slots = 2 aligned pairs (256-bit loads); slots outside
   // [s, e) (an odd run start, the run end) are masked
   uint32_t i0 = w.s & ~1u;
-  while (live) {
-    uint4 r[4];
-    const uint32_t last_pair = (w.e - 1) >> 1;
-    DARE_CHECK(w.s < w.e && w.e <= a.n_samples && (i0 >> 1) <= last_pair);
-    load_pair(recs, i0 >> 1, r[0], r[1]);
-    load_pair(recs, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
-    float bw = 0.0f, bj = 0.0f;
-    // slot i is in the run iff i < e - i0 (and, for slot 0 only, i0 >= s: the
-    // run starts at s or s - 1 rounded down to a pair)
-    const uint32_t rem = w.e - i0;
-    const bool first_ok = i0 >= w.s;
+  auto walk = [&](auto term_mode) {
+    constexpr int TM = decltype(term_mode)::value;
+    while (live) {
+      uint4 r[4];
+      const uint32_t last_pair = (w.e - 1) >> 1;
+      DARE_CHECK(w.s < w.e && w.e <= a.n_samples && (i0 >> 1) <= last_pair);
+      load_pair(recs, i0 >> 1, r[0], r[1]);
+      load_pair(recs, min((i0 >> 1) + 1, last_pair), r[2], r[3]);
+      float bw = 0.0f, bj = 0.0f;
+      // slot i is in the run iff i < e - i0 (and, for slot 0 only, i0 >= s: the
+      // run starts at s or s - 1 rounded down to a pair)
+      const uint32_t rem = w.e - i0;
+      const bool first_ok = i0 >= w.s;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      fast_term<kDistMode, kGate == kGateSplit ? kGateSmem : (kGate == kGateSplitG ? kGateGlobal : kGate)>(
-          r[i], (uint32_t)i < rem && (i > 0 || first_ok),
-                                                                    w, gate, g_single, wh, wl, c2, bw, bj);
-    W += (double)bw;
-    J += (double)bj;
-    i0 += 4;
-    if (i0 >= w.e) {
-      live = open_next();
-      i0 = w.s & ~1u;
+      for (int i = 0; i < 4; ++i)
+        fast_term<kDistMode, TM>(r[i], (uint32_t)i < rem && (i > 0 || first_ok), w, gate, g_single, wh, wl, c2,
+                                 bw, bj);
+      W += (double)bw;
+      J += (double)bj;
+      i0 += 4;
+      if (i0 >= w.e) {
+        live = open_next();
+        i0 = w.s & ~1u;
+      }
     }
+  };
+  if constexpr (kSplitWalk) {
+    if (uni)  // block-uniform
+      walk(std::integral_constant<int, kGateUniform>{});
+    else
+      walk(std::integral_constant<int, kGate == kGateSplit ? kGateSmem : kGateGlobal>{});
+  } else {
+    walk(std::integral_constant<int, kGate>{});
   }
   if (kSplit) {  // the pixel's partial sums (any order: the bound is order-free)
 #pragma unroll
@@ -1164,6 +1184,7 @@ static void launch_reslice(dare_volume_t vol, int32_t P, const double* d_params,
   a.s_records = split ? vol->d_srecords : nullptr;
   a.ocluster = split ? vol->d_ocluster : nullptr;
   a.ncells = vol->ncells;
+  for (int k = 0; k < 6; ++k) a.csingle[k] = split ? vol->split_single[k] : -1;
   const bool sorted = P >= 4 && !brute && !a.pose_major;
   const uint64_t npix = (uint64_t)P * W * H;
   // ambiguity list: 1/16 of the launch's pixels (overflow -> exact recompute of all)

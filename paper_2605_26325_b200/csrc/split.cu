@@ -128,7 +128,11 @@ bool ensure_orient_split(dare_volume_s* vol, cudaStream_t s) {
   for (int k = 0; k < kMaxClusters; ++k) remap[k] = used[k] ? nclu++ : -1;
   if (nclu < 2) return false;
   std::vector<uint8_t> clu(q.size());
-  for (size_t i = 0; i < q.size(); ++i) clu[i] = (uint8_t)remap[raw[i]];
+  int single[kMaxClusters], members[kMaxClusters] = {0, 0, 0, 0, 0, 0};
+  for (size_t i = 0; i < q.size(); ++i) {
+    clu[i] = (uint8_t)remap[raw[i]];
+    if (members[clu[i]]++ == 0) single[clu[i]] = (int)i;
+  }
   const int64_t ncells = vol->ncells, nk = (int64_t)nclu * ncells;
   if (nk + 1 >= (int64_t)INT32_MAX) return false;
   size_t free_b = 0, total_b = 0;
@@ -171,6 +175,7 @@ bool ensure_orient_split(dare_volume_s* vol, cudaStream_t s) {
   vol->d_sbins = d_sbins;
   vol->d_srecords = d_srec;
   vol->split_bytes = need + clu.size();
+  for (int k = 0; k < kMaxClusters; ++k) vol->split_single[k] = k < nclu && members[k] == 1 ? single[k] : -1;
   vol->split_state = 1;
   return true;
 }

@@ -55,6 +55,7 @@ struct dare_volume_s {
   uint8_t* d_ocluster = nullptr;   // n_orient: cluster of each orientation id
   std::atomic<int> split_state{0};  // 0 not tried, 1 built, -1 not applicable
   size_t split_bytes = 0;           // device bytes of the index once built
+  int split_single[6] = {-1, -1, -1, -1, -1, -1};  // per cluster: its only orientation id, or -1
   std::mutex split_mu;
   ~dare_volume_s();
 };
