@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
                                                            uint8_t* __restrict__ nruns,
                                                            unsigned long long* rejected) {
   __shared__ double s_axes[kRunFrames * 9];
-  __shared__ int s_same[kRunFrames];
+  __shared__ uint32_t s_same[kRunFrames / 32];  // bit j: frame j reuses frame j-1's in-plane axes
+  static_assert(kRunFrames == 64 && kRunFrames <= 256, "two ballot words from the first two warps");
   uint32_t u, v;
   tile_pixel(fv, u, v);
   const uint32_t lane = lane_id();
@@ -292,13 +293,16 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
   const int nf = (int)min((uint32_t)kRunFrames, fv.n_frames - f0);
   for (int i = threadIdx.x; i < nf * 9; i += blockDim.x) s_axes[i] = fv.axes[(size_t)f0 * 9 + i];
   __syncthreads();
-  for (int j = threadIdx.x; j < nf; j += blockDim.x) {
-    bool same = j > 0;
+  if (threadIdx.x < kRunFrames) {  // warps 0 and 1: one ballot word each
+    const int j = threadIdx.x;
+    bool same = j > 0 && j < nf;
     for (int c = 0; c < 6 && same; ++c)
       same = __double_as_longlong(s_axes[j * 9 + c]) == __double_as_longlong(s_axes[(j - 1) * 9 + c]);
-    s_same[j] = same;
+    const uint32_t word = __ballot_sync(0xffffffffu, same);
+    if (lane == 0) s_same[j >> 5] = word;
   }
   __syncthreads();
+  const unsigned long long same_bits = (unsigned long long)s_same[0] | ((unsigned long long)s_same[1] << 32);
   const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
   uint2* my = runs + blk * kRunFrames * 256 + threadIdx.x;
   const size_t gb64 = fv.group_base(blockIdx.y);  // (direct mode: 64-bit counters)
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(256, 5) frame_count_tab_k(FrameView fv, CellTa
   for (int j = 0; j < nf; ++j) {  // block-uniform trip count and branches
     const double* fa = s_axes + j * 9;
     double P[3];
-    if (s_same[j]) {
+    if ((same_bits >> j) & 1ull) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) P[a] = S[a] + fa[6 + a];
     } else {
