@@ -116,11 +116,15 @@ def test_reconstruct_random_sweeps_match_oracle(seed, voxel, margin):
     assert_volume_equal(v, oracle.reconstruct(rec, voxel, margin))
 
 
-def test_reconstruct_host_frames_many_upload_groups():
+@pytest.mark.parametrize("buckets", ["0", "1"])
+def test_reconstruct_host_frames_many_upload_groups(buckets, monkeypatch):
     """A linear sweep long enough for several 64-frame chunks: host frames upload in groups and
     the fill runs one launch per group; frames on the device take one fill launch.  Both equal
-    the oracle (insertion order across chunk and group boundaries)."""
+    the oracle (insertion order across chunk and group boundaries), with the per-cell and the
+    bucketed fill (bucket cursors carried across the group launches)."""
     import torch
+
+    monkeypatch.setenv("DARE_FILL_BUCKETS", buckets)
 
     rng = np.random.default_rng(17)
     n, h, w = 300, 12, 14
