@@ -11,6 +11,16 @@
 // NegLn2loN, r); tmp = fma(r2*r2, fma(r,C5,C4), fma(fma(r,C3,C2), r2, r+tail));
 // result = fma(scale, tmp, scale)) makes every weight bit-identical.
 // tests/test_exp_port.py pins this against the host libm.
+//
+// Provenance and licence: the algorithm, the polynomial coefficients and the
+// 2^(k/128) table follow glibc's sysdeps/ieee754/dbl-64/e_exp.c and
+// e_exp_data.c (glibc 2.39; code contributed by Arm Ltd, "Copyright (C)
+// 2018-2024 Free Software Foundation, Inc."), distributed under the GNU
+// Lesser General Public License v2.1 or later.  The table here is not copied
+// from those sources: tools/gen_exp_table.py regenerates it from the defining
+// identity (exp_table.h); the constants are the published ones.  Users
+// redistributing this file take the LGPL-2.1+ terms of that algorithm into
+// account.
 #pragma once
 #include <stdint.h>
 #include <string.h>
